@@ -1,0 +1,316 @@
+#!/usr/bin/env python
+"""GSGP generations/sec on B200 — the BASELINE.json metric.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
+
+A step is one GSGP generation (plan -> fused GSM+SSE on train and test ->
+SSE reduction -> [NCCL allreduce] -> elitist survival) over the configured
+synthetic workload.  W warm-up generations run untimed, then exactly K
+generations are timed on the device with CUDA events (the engine records
+the window events on its stream).  Default workload: C3 = pop 1024, 8
+features, 10M train + 2.5M test cases, random-tree pool 1024, k=1024 — the
+configuration the metric is quoted on at 1/2/4/8 B200 (cases sharded by
+rank, strong scaling); it fits one GPU (~103 GB).
+
+Printed JSON line (rank 0): value = generations/s of the whole job; e2e =
+the same metric through the public `run_evolution` call from host numpy
+datasets (H2D, init, loop and D2H inside the timed region); roofline = the
+fused GSM+SSE kernel's algorithmic bytes (4*N*(2m+D_g+1) per
+generation) over its CUDA-event time; cpu_baseline = the reference loop
+(oracle port) on this host's cores.  `--impl reference` times that CPU
+reference path alone, in bounded per-step samples.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    "c1": dict(m=256, r=1024, k=1024, l=5, ntr=500, nte=200, g=50,
+               desc="C1 synthetic SR, 5 features, 500/200 cases, pop 256, pool 1024, k=1024"),
+    "c2": dict(m=1024, r=1024, k=1024, l=8, ntr=100_000, nte=25_000, g=500,
+               desc="C2 pop 1024, 8 features, 100k+25k cases, pool 1024, k=1024"),
+    "c3": dict(m=1024, r=1024, k=1024, l=8, ntr=10_000_000, nte=2_500_000, g=100,
+               desc="C3 pop 1024, 8 features, 10M+2.5M cases sharded by case, pool 1024, k=1024"),
+    "c4": dict(m=8192, r=1024, k=255, l=8, ntr=1_000_000, nte=250_000, g=50,
+               desc="C4 pop 8192, 1M+250k cases, pool 1024, k=255 (depth-8 trees)"),
+    "c5": dict(m=2048, r=1024, k=1024, l=100, ntr=2_000_000, nte=500_000, g=50,
+               desc="C5 pop 2048, 100 features, 2M+500k cases, pool 1024, k=1024"),
+}
+METRIC = "generations/sec"
+NVML_REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+                0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+                0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+                0x100: "display_clock_setting"}
+
+
+def peaks():
+    try:
+        d = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler(threading.Thread):
+    """nvidia-smi-equivalent sampling (NVML) of SM clock and throttle reasons."""
+
+    def __init__(self, index: int, period: float = 0.02):
+        super().__init__(daemon=True)
+        self.index, self.period = index, period
+        self.samples = []
+        self.stop_flag = threading.Event()
+        self.max_mhz = None
+        self.ok = True
+
+    def run(self):
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            get_reasons = getattr(N, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                N.nvmlDeviceGetCurrentClocksThrottleReasons
+            while not self.stop_flag.is_set():
+                util = N.nvmlDeviceGetUtilizationRates(h).gpu
+                self.samples.append((N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM), int(get_reasons(h)), util))
+                time.sleep(self.period)
+        except Exception as exc:  # no NVML: report what we have
+            self.ok = False
+            self.err = repr(exc)
+
+    def summary(self):
+        self.stop_flag.set()
+        self.join(timeout=2)
+        load = [s for s in self.samples if s[2] >= 30] or self.samples
+        reasons = set()
+        for _, bits, _ in load:
+            for bit, name in NVML_REASONS.items():
+                if bits & bit and name != "gpu_idle":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median([s[0] for s in load]) if load else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(reasons),
+                "samples": len(self.samples), "samples_under_load": len(load)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return world, rank, local
+
+
+def bytes_per_generation(plans, N: int, m: int) -> np.ndarray:
+    """4*N*(2m + D_g + 1), D_g = distinct pool rows of the plan."""
+    out = []
+    for u, v in plans:
+        D = len(np.union1d(u, v))
+        out.append(4.0 * N * (2 * m + D + 1))
+    return np.array(out)
+
+
+def cpu_leg(c, budget_s: float):
+    from oracle import cpu_bench
+    t = cpu_bench.time_loop(c["m"], c["r"], c["ntr"], c["nte"], budget_s=budget_s,
+                            max_cases=125_000, workers=os.cpu_count())
+    N = c["ntr"] + c["nte"]
+    sample = (f"reference generation body (oracle port of gsgp/evolution.py:146-158, numpy, "
+              f"{t['workers']} threads) on synthetic fp64 state m={c['m']} r={c['r']} with "
+              f"{t['sample_train']}+{t['sample_test']} cases, {t['gens_timed']} timed generations")
+    if t["case_fraction"] < 1.0:
+        sample += f", rate scaled linearly from {t['sample_train'] + t['sample_test']} to {N} cases"
+    return {"value": t["gen_per_s"], "unit": METRIC, "cores": t["workers"], "kind": "port",
+            "sample": sample, "cpu": cpu_bench.cpu_model(),
+            "sec_per_gen_sample": t["sec_per_gen_sample"]}
+
+
+def run_ours(args):
+    world, rank, local = dist_env()
+    td = None
+    if world > 1:
+        import torch.distributed as td
+        td.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2106_04034_b200 as G
+    from paper_2106_04034_b200 import _lib, dist
+    lib = _lib.load()
+    _lib.check(lib.gsgp_set_device(local))
+    if world > 1:
+        dist.init_from_torch()
+
+    def barrier():
+        if td:
+            td.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if not td:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64)
+        td.all_reduce(t, op=td.ReduceOp.MAX)
+        return float(t.item())
+
+    c = CONFIGS[args.config]
+    K, W = args.steps, args.warmup
+    train = G.make_benchmark_dataset(c["ntr"], c["l"], seed=1)
+    test = G.make_benchmark_dataset(c["nte"], c["l"], seed=2)
+    cfg = G.RunConfig(population_size=c["m"], random_trees=c["r"], program_size=c["k"],
+                      generations=W + K, seed=1)
+
+    # ---- device-timed run: W warm-up generations, then exactly K timed
+    sampler = ClockSampler(local)
+    sampler.start()
+    barrier()
+    res = G.run_evolution(cfg, train, test, time_kernels=True, window_start=W)
+    barrier()
+    clocks = sampler.summary()
+    win_ms = max_over_ranks(res.device["window_ms"])
+    value = K / (win_ms / 1e3)
+
+    lo, hi = res.device["shard_train_range"]
+    te_lo, te_hi = dist.shard_range(c["nte"], world, rank)
+    n_local = (hi - lo) + (te_hi - te_lo)     # cases this rank's kernel streams
+    plans = [(e.plan.u, e.plan.v) for e in res.lineage.entries[W:]]
+    bpg = bytes_per_generation(plans, n_local, c["m"])
+    gsm_ms = res.device["window_gsm_ms"]
+    launches = max(res.device["window_gsm_launches"], 1)
+    achieved = float(bpg.sum() / (gsm_ms / 1e3) / 1e9)
+    peak, peak_kind = peaks()
+    traffic = None
+    tfile = ROOT / "profiles" / "gsm_traffic.json"
+    if tfile.exists():
+        try:
+            traffic = json.loads(tfile.read_text()).get(args.config)
+        except Exception:
+            traffic = None
+
+    # ---- end to end through the public API (host datasets, H2D/D2H inside)
+    e2e = None
+    if not args.no_e2e:
+        cfg2 = G.RunConfig(population_size=c["m"], random_trees=c["r"], program_size=c["k"],
+                           generations=K, seed=1)
+        barrier()
+        t0 = time.perf_counter()
+        res2 = G.run_evolution(cfg2, train, test)
+        barrier()
+        wall = max_over_ranks(time.perf_counter() - t0)
+        h2d = (train.features.nbytes + train.target.nbytes + test.features.nbytes + test.target.nbytes)
+        d2h = (K + 1) * (8 + 8 + 1 + 8 + 8 + 8) + K * c["m"] * 24 + 8 * c["ntr"]
+        e2e = {"value": K / wall, "unit": METRIC, "h2d_bytes_per_step": h2d / K,
+               "d2h_bytes_per_step": d2h / K, "wall_s": wall,
+               "init_ms": res2.timings.create_population_ms + res2.timings.compute_semantics_ms,
+               "loop_ms": res2.timings.evolution_ms}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_leg(c, args.cpu_budget)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "generations/s", "n_gpus": world,
+            "steps": K, "warmup": W, "ms_per_step": win_ms / K, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32 storage / f64 interp+SSE",
+            "data": "synthetic (make_benchmark_dataset: U[-1,1) features, x0*x1+sum(x) target)",
+            "config": {"workload": c["desc"], "m": c["m"], "r": c["r"], "k": c["k"],
+                       "features": c["l"], "n_train": c["ntr"], "n_test": c["nte"],
+                       "parallelism": f"case-shard x{world}",
+                       "l2": "inputs larger than L2 (population and pool semantics "
+                             f"{4 * c['m'] * (c['ntr'] + c['nte']) / 1e9:.1f} GB each)"
+                       if c["ntr"] > 1_000_000 else "small config: L2-resident"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "k_gsm<float> (fused GSM+SSE, train+test)",
+                         "peak_kind": peak_kind,
+                         "algorithmic_bytes_per_launch": float(bpg.mean()),
+                         "avg_launch_ms": gsm_ms / launches,
+                         "kernel_share_of_step": gsm_ms / win_ms},
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "gpu_launches": res.device["window_loop_launches"],
+            "clocks": clocks,
+            "init_ms": {"create_population": res.timings.create_population_ms,
+                        "compute_semantics": res.timings.compute_semantics_ms},
+            "graph_mode_note": "timed run uses direct launches with per-kernel events",
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy()
+        td.destroy_process_group()
+
+
+def run_reference(args):
+    """CPU reference path (oracle port: the reference is pure Python and has
+    no compiled form) on this host's cores; each step is one reference
+    generation over a bounded case sample, value scaled to the full config."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import cpu_bench
+    c = CONFIGS[args.config]
+    K, W = args.steps, args.warmup
+    N = c["ntr"] + c["nte"]
+    workers = os.cpu_count() or 1
+    # probe the per-case cost, then size a step to ~min(0.5 s, 150 s / (K+W))
+    probe_cases = min(N, 20_000)
+    p = cpu_bench.time_loop(c["m"], c["r"], int(probe_cases * 0.8), probe_cases - int(probe_cases * 0.8),
+                            budget_s=0.0, workers=workers, min_gens=1, warmup=1)
+    step_s = min(0.5, 150.0 / max(K + W, 1))
+    n_s = min(N, cpu_bench.sample_cases_for(step_s, c["m"], (probe_cases, p["sec_per_gen_sample"])))
+    s_tr = max(1, int(round(n_s * c["ntr"] / N)))
+    s_te = max(1, n_s - s_tr)
+    st = cpu_bench.LoopState(c["m"], c["r"], s_tr, s_te)
+    for w in range(W):
+        st.generation(w + 1, workers=workers)
+    t0 = time.perf_counter()
+    for k in range(K):
+        st.generation(W + k + 1, workers=workers)
+    dt = time.perf_counter() - t0
+    frac = (s_tr + s_te) / N
+    value = K / dt * frac
+    sample = (f"each step = one reference generation (oracle port of gsgp/evolution.py:146-158, "
+              f"numpy, {workers} threads) over a {s_tr}+{s_te}-case sample of the {N}-case "
+              f"workload; value = steps/s x {frac:.6f} (full-generation equivalents)")
+    line = {"metric": METRIC, "value": value, "unit": "generations/s", "n_gpus": world,
+            "steps": K, "warmup": W, "ms_per_step": dt / K * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": c["desc"], "m": c["m"], "r": c["r"], "k": c["k"],
+                       "features": c["l"], "n_train": c["ntr"], "n_test": c["nte"]},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": METRIC, "cores": workers, "kind": "port",
+                             "sample": sample, "cpu": cpu_bench.cpu_model()},
+            "e2e": {"value": value, "unit": METRIC, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

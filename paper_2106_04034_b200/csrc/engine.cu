@@ -1,0 +1,524 @@
+// run_evolution on the device (gsgp/evolution.py:100-179).
+//
+// Host side of the engine: allocation, case sharding, the one-time init
+// (CreatePopulation -> compile -> interpret population + pool -> initial
+// fitness) and the generation loop, which is a fixed sequence of kernels
+//   plan -> GSM+SSE (per shard) -> SSE tile reduction -> [shard sum] ->
+//   [NCCL allreduce over ranks] -> survival
+// whose every decision lives on the device (control block), so one captured
+// generation is replayed g times as a CUDA graph.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "gsgp_b200.h"
+#include "kernels.cuh"
+
+namespace gsgp {
+
+// ------------------------------------------------------------- device memory
+struct DevBuf {
+  void* p = nullptr;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+  }
+  void alloc(size_t bytes) {
+    release();
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      throw Error{e == cudaErrorMemoryAllocation ? ERR_OOM : ERR_CUDA,
+                  "cudaMalloc(" + std::to_string(bytes) + " bytes): " + cudaGetErrorString(e)};
+    }
+  }
+  template <typename T> T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+struct Event {
+  cudaEvent_t e = nullptr;
+  Event() { GSGP_CUDA(cudaEventCreate(&e)); }
+  ~Event() { if (e) cudaEventDestroy(e); }
+  Event(const Event&) = delete;
+  Event& operator=(const Event&) = delete;
+};
+
+float elapsed_ms(const Event& a, const Event& b) {
+  float t = 0.f;
+  GSGP_CUDA(cudaEventElapsedTime(&t, a.e, b.e));
+  return t;
+}
+
+// ---------------------------------------------------------- NCCL (dlopen)
+struct NcclApi {
+  void* h = nullptr;
+  decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+  decltype(&ncclCommInitRank) commInitRank = nullptr;
+  decltype(&ncclAllReduce) allReduce = nullptr;
+  decltype(&ncclCommDestroy) commDestroy = nullptr;
+  decltype(&ncclGetErrorString) errStr = nullptr;
+
+  void load() {
+    if (h) return;
+    // prefer an already-loaded libnccl (e.g. torch's); RTLD_NOLOAD first
+    h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) throw Error{ERR_NCCL, std::string("cannot load libnccl.so.2: ") + dlerror()};
+    getUniqueId = (decltype(getUniqueId))dlsym(h, "ncclGetUniqueId");
+    commInitRank = (decltype(commInitRank))dlsym(h, "ncclCommInitRank");
+    allReduce = (decltype(allReduce))dlsym(h, "ncclAllReduce");
+    commDestroy = (decltype(commDestroy))dlsym(h, "ncclCommDestroy");
+    errStr = (decltype(errStr))dlsym(h, "ncclGetErrorString");
+    if (!getUniqueId || !commInitRank || !allReduce || !commDestroy || !errStr)
+      throw Error{ERR_NCCL, "libnccl.so.2 lacks required symbols"};
+  }
+  void check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) throw Error{ERR_NCCL, std::string(what) + ": " + errStr(r)};
+  }
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  return api;
+}
+
+struct CommState {
+  ncclComm_t comm = nullptr;
+  int world = 1, rank = 0;
+};
+CommState& comm_state() {
+  static CommState c;
+  return c;
+}
+
+void comm_unique_id(unsigned char* id) {
+  nccl().load();
+  ncclUniqueId u;
+  nccl().check(nccl().getUniqueId(&u), "ncclGetUniqueId");
+  std::memcpy(id, u.internal, NCCL_UNIQUE_ID_BYTES);
+}
+
+void comm_init(int world, int rank, const unsigned char* id) {
+  GSGP_REQUIRE(world >= 1 && rank >= 0 && rank < world, "bad world/rank");
+  CommState& c = comm_state();
+  if (c.comm) {
+    nccl().commDestroy(c.comm);
+    c.comm = nullptr;
+  }
+  c.world = world;
+  c.rank = rank;
+  if (world == 1) return;
+  nccl().load();
+  ncclUniqueId u;
+  std::memcpy(u.internal, id, NCCL_UNIQUE_ID_BYTES);
+  nccl().check(nccl().commInitRank(&c.comm, world, u, rank), "ncclCommInitRank");
+}
+
+void comm_destroy() {
+  CommState& c = comm_state();
+  if (c.comm) nccl().commDestroy(c.comm);
+  c.comm = nullptr;
+  c.world = 1;
+  c.rank = 0;
+}
+
+void shard_range(int64_t n, int64_t count, int64_t index, int64_t* lo, int64_t* hi) {
+  *lo = (n * index) / count;
+  *hi = (n * (index + 1)) / count;
+}
+
+// ------------------------------------------------------------- small kernels
+namespace {
+
+__global__ void k_transpose(const double* __restrict__ Xr, int64_t N, int l, double* __restrict__ XT) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= N * l) return;
+  int64_t q = e / l, f = e - q * l;
+  XT[f * N + q] = Xr[e];
+}
+
+__global__ void k_wide_split(const int32_t* wide, int64_t m, int32_t* bits) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  bits[2 * i] = wide[i] & 1;
+  bits[2 * i + 1] = (wide[i] >> 1) & 1;
+}
+
+__global__ void k_wide_merge(const int32_t* bits, int64_t m, int32_t* wide) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  wide[i] = (bits[2 * i] > 0 ? 1 : 0) | (bits[2 * i + 1] > 0 ? 2 : 0);
+}
+
+inline unsigned nblk(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t > 0 ? (n + t - 1) / t : 1); }
+
+}  // namespace
+
+// --------------------------------------------------------------------- run
+struct Shard {
+  int64_t tr_lo = 0, tr_hi = 0, te_lo = 0, te_hi = 0;
+  int64_t ntr = 0, nte = 0, pitch = 0, test_off = 0, ntiles = 0;
+  DevBuf S, pool, elite[2], y_store, part, sse;
+};
+
+void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, int64_t ntr,
+                const double* Xte, const double* yte, int64_t nte, int32_t l, gsgp_outputs* out) {
+  auto t_host0 = std::chrono::steady_clock::now();
+  GSGP_REQUIRE(cfg && out, "null config/outputs");
+  const int64_t m = cfg->population_size, r = cfg->random_trees, k = cfg->program_size,
+                g = cfg->generations;
+  GSGP_REQUIRE(m >= 1 && r >= 1 && k >= 1, "population_size, random_trees, program_size must be >= 1");
+  GSGP_REQUIRE(g >= 0, "generations must be >= 0");
+  GSGP_REQUIRE(r >= 2 || g == 0, "geometric semantic mutation needs at least 2 random trees");
+  GSGP_REQUIRE(ntr >= 1 && nte >= 1 && l >= 1, "datasets must have at least one row and one feature");
+  GSGP_REQUIRE(l <= 65535, "at most 65535 features");
+  GSGP_REQUIRE(k < (1ll << 24), "program_size too large");
+  const double total = cfg->p_function + cfg->p_feature + cfg->p_constant;
+  GSGP_REQUIRE(cfg->p_function >= 0 && cfg->p_feature >= 0 && cfg->p_constant >= 0 && total > 0,
+               "gene probabilities must be non-negative with positive sum");
+  GSGP_REQUIRE(cfg->division_eps > 0, "division_eps must be > 0");
+  const bool f64 = cfg->storage_f64 != 0;
+  const size_t esz = f64 ? 8 : 4;
+  const int G = cfg->virtual_shards < 1 ? 1 : cfg->virtual_shards;
+  GSGP_REQUIRE(G <= 16, "at most 16 virtual shards");
+  CommState& cs = comm_state();
+  const int W = cs.world;
+  const int64_t nsh_total = (int64_t)W * G;
+
+  cudaStream_t st;
+  GSGP_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  struct StreamGuard {
+    cudaStream_t s;
+    ~StreamGuard() { cudaStreamDestroy(s); }
+  } sg{st};
+
+  Event ev_begin, ev_created, ev_sem, ev_loop0, ev_loop1;
+  GSGP_CUDA(cudaEventRecord(ev_begin.e, st));
+
+  // ---- shards and per-shard device data
+  std::vector<std::unique_ptr<Shard>> sh;
+  for (int s = 0; s < G; ++s) {
+    auto p = std::make_unique<Shard>();
+    const int64_t gs = (int64_t)cs.rank * G + s;
+    shard_range(ntr, nsh_total, gs, &p->tr_lo, &p->tr_hi);
+    shard_range(nte, nsh_total, gs, &p->te_lo, &p->te_hi);
+    p->ntr = p->tr_hi - p->tr_lo;
+    p->nte = p->te_hi - p->te_lo;
+    p->test_off = pad32(p->ntr);
+    p->pitch = p->test_off + pad32(p->nte);
+    p->ntiles = gsm_tiles(p->pitch, f64);
+    sh.push_back(std::move(p));
+  }
+  out->shard_train_lo = sh.front()->tr_lo;
+  out->shard_train_hi = sh.back()->tr_hi;
+
+  // ---- global (replicated) state
+  DevBuf tags, codes, consts, ins, plen, pdepth, pmax, scratch, flags, cval;
+  const int64_t ng = m + r;
+  tags.alloc(ng * k);
+  codes.alloc(ng * k * 4);
+  consts.alloc(ng * k * 8);
+  ins.alloc(ng * (k + 1) * sizeof(Ins));
+  plen.alloc(ng * 4);
+  pdepth.alloc(ng * 4);
+  pmax.alloc(4);
+  scratch.alloc(ng * 4 * k * 4);
+  flags.alloc(ng * k);
+  cval.alloc(ng * k * 8);
+  DevBuf F, TS, Fo, To, wide, ctl, sse_total, nonfinite;
+  F.alloc(m * 8); TS.alloc(m * 8); Fo.alloc(m * 8); To.alloc(m * 8);
+  wide.alloc(m * 4);
+  ctl.alloc(CTL_WORDS * 8);
+  sse_total.alloc(m * 2 * 8);
+  nonfinite.alloc(8);
+  GSGP_CUDA(cudaMemsetAsync(wide.p, 0, m * 4, st));
+  GSGP_CUDA(cudaMemsetAsync(ctl.p, 0, CTL_WORDS * 8, st));
+  GSGP_CUDA(cudaMemsetAsync(nonfinite.p, 0, 8, st));
+  DevBuf pu, pv, pms, rsrc, ridx, rslot, rfit, ttr, tte;
+  const int64_t gm = (g > 0 ? g : 1) * m;
+  pu.alloc(gm * 8); pv.alloc(gm * 8); pms.alloc(gm * 8);
+  rsrc.alloc(g + 1); ridx.alloc((g + 1) * 8); rslot.alloc((g + 1) * 8); rfit.alloc((g + 1) * 8);
+  ttr.alloc((g + 1) * 8); tte.alloc((g + 1) * 8);
+
+  // ---- CreatePopulation (population.py:73-92; evolution.py:117-118)
+  GeneParams gp;
+  gp.seed = cfg->seed;
+  gp.thr_fun = cfg->p_function / total;
+  gp.thr_feat = gp.thr_fun + cfg->p_feature / total;
+  gp.erc_low = cfg->erc_low;
+  gp.erc_high = cfg->erc_high;
+  gp.n_features = l;
+  gp.k = (int32_t)k;
+  launch_create_population(gp, m, 0, tags.as<uint8_t>(), codes.as<int32_t>(), consts.as<double>(), st);
+  launch_create_population(gp, r, (uint64_t)m, tags.as<uint8_t>() + m * k, codes.as<int32_t>() + m * k,
+                           consts.as<double>() + m * k, st);
+  GSGP_CUDA(cudaEventRecord(ev_created.e, st));
+
+  // ---- compile all m + r genomes once
+  Program prog{ins.as<Ins>(), plen.as<int32_t>(), pdepth.as<int32_t>(), pmax.as<int32_t>(),
+               scratch.as<int32_t>(), flags.as<uint8_t>(), cval.as<double>()};
+  launch_compile(tags.as<uint8_t>(), codes.as<int32_t>(), consts.as<double>(), ng, (int32_t)k,
+                 cfg->division_eps, prog, st);
+  int32_t maxdepth = 0;
+  GSGP_CUDA(cudaMemcpyAsync(&maxdepth, pmax.p, 4, cudaMemcpyDeviceToHost, st));
+  GSGP_CUDA(cudaStreamSynchronize(st));
+
+  // ---- per shard: upload the case slice, interpret population and pool
+  for (auto& p : sh) {
+    const int64_t N = p->ntr + p->nte;
+    p->S.alloc(m * p->pitch * esz);
+    p->pool.alloc(r * p->pitch * esz);
+    p->elite[0].alloc(p->pitch * esz);
+    p->elite[1].alloc(p->pitch * esz);
+    p->y_store.alloc(p->pitch * 8);
+    p->part.alloc(m * p->ntiles * 2 * 8);
+    p->sse.alloc(m * 2 * 8);
+    GSGP_CUDA(cudaMemsetAsync(p->S.p, 0, m * p->pitch * esz, st));
+    GSGP_CUDA(cudaMemsetAsync(p->pool.p, 0, r * p->pitch * esz, st));
+    GSGP_CUDA(cudaMemsetAsync(p->elite[0].p, 0, p->pitch * esz, st));
+    GSGP_CUDA(cudaMemsetAsync(p->elite[1].p, 0, p->pitch * esz, st));
+    GSGP_CUDA(cudaMemsetAsync(p->y_store.p, 0, p->pitch * 8, st));
+    GSGP_CUDA(cudaMemsetAsync(p->sse.p, 0, m * 2 * 8, st));
+    if (N == 0) continue;
+    GSGP_CUDA(cudaMemcpyAsync(p->y_store.as<double>(), ytr + p->tr_lo, p->ntr * 8, cudaMemcpyHostToDevice, st));
+    GSGP_CUDA(cudaMemcpyAsync(p->y_store.as<double>() + p->test_off, yte + p->te_lo, p->nte * 8,
+                              cudaMemcpyHostToDevice, st));
+    DevBuf Xr, XT, ystack;
+    Xr.alloc(N * l * 8);
+    XT.alloc(N * l * 8);
+    ystack.alloc(N * 8);
+    GSGP_CUDA(cudaMemcpyAsync(Xr.as<double>(), Xtr + p->tr_lo * l, p->ntr * l * 8, cudaMemcpyHostToDevice, st));
+    GSGP_CUDA(cudaMemcpyAsync(Xr.as<double>() + p->ntr * l, Xte + p->te_lo * l, p->nte * l * 8,
+                              cudaMemcpyHostToDevice, st));
+    GSGP_CUDA(cudaMemcpyAsync(ystack.as<double>(), ytr + p->tr_lo, p->ntr * 8, cudaMemcpyHostToDevice, st));
+    GSGP_CUDA(cudaMemcpyAsync(ystack.as<double>() + p->ntr, yte + p->te_lo, p->nte * 8,
+                              cudaMemcpyHostToDevice, st));
+    k_transpose<<<nblk(N * l), 256, 0, st>>>(Xr.as<double>(), N, l, XT.as<double>());
+    GSGP_CUDA(cudaGetLastError());
+
+    InterpArgs ia{};
+    ia.code = ins.as<Ins>();
+    ia.len = plen.as<int32_t>();
+    ia.k1 = k + 1;
+    ia.count = m;
+    ia.XT = XT.as<double>();
+    ia.xt_pitch = N;
+    ia.l = l;
+    ia.ntr = p->ntr;
+    ia.nte = p->nte;
+    ia.eps = cfg->division_eps;
+    ia.maxdepth = maxdepth;
+    ia.out = p->S.p;
+    ia.out_is_f64 = f64 ? 1 : 0;
+    ia.pitch = p->pitch;
+    ia.test_off = p->test_off;
+    ia.y = ystack.as<double>();
+    ia.wide = wide.as<int32_t>();
+    ia.nonfinite = nonfinite.as<unsigned long long>();
+    const int64_t itiles = interp_tiles(ia, nullptr);
+    DevBuf ipart;
+    ipart.alloc(m * itiles * 2 * 8);
+    ia.part = ipart.as<double>();
+    launch_interpret(ia, INTERP_POP, st);
+    launch_reduce_partials(ipart.as<double>(), m, itiles, p->sse.as<double>(), false, st);
+    // pool: stream base m, same compiled program buffer offset by m genomes
+    InterpArgs ip = ia;
+    ip.code = ins.as<Ins>() + m * (k + 1);
+    ip.len = plen.as<int32_t>() + m;
+    ip.count = r;
+    ip.out = p->pool.p;
+    ip.part = nullptr;
+    ip.wide = nullptr;
+    ip.y = nullptr;
+    launch_interpret(ip, INTERP_POOL, st);
+    GSGP_CUDA(cudaStreamSynchronize(st));   // temporaries (Xr, XT, ipart) are freed on scope exit
+  }
+
+  // ---- exchange the initial SSE / overflow flags across shards and ranks
+  // G == 1: survival reads shard 0's SSE vector directly (no copy)
+  double* sse_vec = G == 1 ? sh[0]->sse.as<double>() : sse_total.as<double>();
+  auto exchange = [&](cudaStream_t s) {
+    if (G > 1) {
+      std::vector<const double*> v;
+      for (auto& p : sh) v.push_back(p->sse.as<double>());
+      launch_sum_shards(v.data(), G, m * 2, sse_vec, s);
+    }
+    if (W > 1)
+      nccl().check(nccl().allReduce(sse_vec, sse_vec, m * 2, ncclFloat64, ncclSum, cs.comm, s),
+                   "ncclAllReduce(sse)");
+  };
+  exchange(st);
+  if (W > 1) {
+    DevBuf bits;
+    bits.alloc(m * 2 * 4);
+    k_wide_split<<<nblk(m), 256, 0, st>>>(wide.as<int32_t>(), m, bits.as<int32_t>());
+    nccl().check(nccl().allReduce(bits.p, bits.p, m * 2, ncclInt32, ncclSum, cs.comm, st), "ncclAllReduce(wide)");
+    k_wide_merge<<<nblk(m), 256, 0, st>>>(bits.as<int32_t>(), m, wide.as<int32_t>());
+    nccl().check(nccl().allReduce(nonfinite.p, nonfinite.p, 1, ncclUint64, ncclSum, cs.comm, st),
+                 "ncclAllReduce(overflow)");
+    GSGP_CUDA(cudaStreamSynchronize(st));
+  }
+
+  SurviveArgs sa{};
+  sa.m = m;
+  sa.ntr = (double)ntr;
+  sa.nte = (double)nte;
+  sa.sse_off = sse_vec;
+  sa.F = F.as<double>();
+  sa.TS = TS.as<double>();
+  sa.wide = wide.as<int32_t>();
+  sa.Fo = Fo.as<double>();
+  sa.To = To.as<double>();
+  sa.ctl = ctl.as<int64_t>();
+  sa.rec_src = rsrc.as<int8_t>();
+  sa.rec_idx = ridx.as<int64_t>();
+  sa.rec_slot = rslot.as<int64_t>();
+  sa.rec_fit = rfit.as<double>();
+  sa.trace_tr = ttr.as<double>();
+  sa.trace_te = tte.as<double>();
+  launch_init_state(sa, st);
+  GSGP_CUDA(cudaEventRecord(ev_sem.e, st));
+
+  // ---- generation loop (evolution.py:146-158)
+  PlanParams pp{cfg->seed, m, r, cfg->mutation_step_uniform, cfg->mutation_step};
+  const bool timed = cfg->time_kernels != 0;
+  std::vector<std::unique_ptr<Event>> tev;
+  int64_t launches_per_gen = 0;
+  auto enqueue_generation = [&](cudaStream_t s, Event* t0, Event* t1) {
+    int64_t n = 0;
+    launch_plan(pp, 0, ctl.as<int64_t>(), pu.as<int64_t>(), pv.as<int64_t>(), pms.as<double>(), m, s);
+    ++n;
+    if (t0) GSGP_CUDA(cudaEventRecord(t0->e, s));
+    for (auto& p : sh) {
+      if (p->pitch == 0) continue;
+      GsmArgs a{};
+      a.pool = p->pool.p;
+      a.S = p->S.p;
+      a.elite_prev = p->elite[0].p;
+      a.elite_cur = p->elite[1].p;
+      a.y = p->y_store.as<double>();
+      a.pitch = p->pitch;
+      a.test_off = p->test_off;
+      a.m = m;
+      a.u = pu.as<int64_t>();
+      a.v = pv.as<int64_t>();
+      a.ms = pms.as<double>();
+      a.ctl = ctl.as<int64_t>();
+      a.sign = cfg->gsm_sign;
+      a.part = p->part.as<double>();
+      launch_gsm(a, f64, false, s);
+      ++n;
+    }
+    if (t1) GSGP_CUDA(cudaEventRecord(t1->e, s));
+    for (auto& p : sh) {
+      if (p->pitch == 0) continue;
+      launch_reduce_partials(p->part.as<double>(), m, p->ntiles, p->sse.as<double>(), false, s);
+      ++n;
+    }
+    exchange(s);
+    n += (G > 1) ? 1 : 0;
+    launch_survive(sa, s);
+    ++n;
+    launches_per_gen = n;
+  };
+  // timing window: generations (w0, g]; ev_win0 is recorded after generation w0
+  const int64_t w0 = cfg->window_start < 0 ? 0 : (cfg->window_start > g ? g : cfg->window_start);
+  Event ev_win0;
+  GSGP_CUDA(cudaEventRecord(ev_loop0.e, st));
+  if (w0 == 0) GSGP_CUDA(cudaEventRecord(ev_win0.e, st));
+  double gsm_ms = 0.0, win_gsm_ms = 0.0;
+  if (g > 0) {
+    cudaGraphExec_t exec = nullptr;
+    cudaGraph_t graph = nullptr;
+    if (!timed && cfg->use_graph) {
+      GSGP_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      enqueue_generation(st, nullptr, nullptr);
+      GSGP_CUDA(cudaStreamEndCapture(st, &graph));
+      GSGP_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    }
+    if (timed)
+      for (int64_t t = 0; t < 2 * g; ++t) tev.push_back(std::make_unique<Event>());
+    for (int64_t t = 0; t < g; ++t) {
+      if (timed) enqueue_generation(st, tev[2 * t].get(), tev[2 * t + 1].get());
+      else if (exec) GSGP_CUDA(cudaGraphLaunch(exec, st));
+      else enqueue_generation(st, nullptr, nullptr);
+      if (t + 1 == w0) GSGP_CUDA(cudaEventRecord(ev_win0.e, st));
+    }
+    GSGP_CUDA(cudaEventRecord(ev_loop1.e, st));
+    GSGP_CUDA(cudaStreamSynchronize(st));
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+  } else {
+    GSGP_CUDA(cudaEventRecord(ev_loop1.e, st));
+  }
+  GSGP_CUDA(cudaStreamSynchronize(st));
+  if (timed)
+    for (int64_t t = 0; t < g; ++t) {
+      const double d = elapsed_ms(*tev[2 * t], *tev[2 * t + 1]);
+      gsm_ms += d;
+      if (t >= w0) win_gsm_ms += d;
+    }
+
+  // ---- results back to the host
+  GSGP_CUDA(cudaMemcpyAsync(out->train_trace, ttr.p, (g + 1) * 8, cudaMemcpyDeviceToHost, st));
+  GSGP_CUDA(cudaMemcpyAsync(out->test_trace, tte.p, (g + 1) * 8, cudaMemcpyDeviceToHost, st));
+  GSGP_CUDA(cudaMemcpyAsync(out->elite_src, rsrc.p, g + 1, cudaMemcpyDeviceToHost, st));
+  GSGP_CUDA(cudaMemcpyAsync(out->elite_idx, ridx.p, (g + 1) * 8, cudaMemcpyDeviceToHost, st));
+  GSGP_CUDA(cudaMemcpyAsync(out->elite_slot, rslot.p, (g + 1) * 8, cudaMemcpyDeviceToHost, st));
+  GSGP_CUDA(cudaMemcpyAsync(out->elite_fit, rfit.p, (g + 1) * 8, cudaMemcpyDeviceToHost, st));
+  if (g > 0 && out->plan_u) GSGP_CUDA(cudaMemcpyAsync(out->plan_u, pu.p, g * m * 8, cudaMemcpyDeviceToHost, st));
+  if (g > 0 && out->plan_v) GSGP_CUDA(cudaMemcpyAsync(out->plan_v, pv.p, g * m * 8, cudaMemcpyDeviceToHost, st));
+  if (g > 0 && out->plan_ms) GSGP_CUDA(cudaMemcpyAsync(out->plan_ms, pms.p, g * m * 8, cudaMemcpyDeviceToHost, st));
+  int64_t hctl[CTL_WORDS];
+  unsigned long long hnf = 0;
+  GSGP_CUDA(cudaMemcpyAsync(hctl, ctl.p, sizeof(hctl), cudaMemcpyDeviceToHost, st));
+  GSGP_CUDA(cudaMemcpyAsync(&hnf, nonfinite.p, 8, cudaMemcpyDeviceToHost, st));
+  GSGP_CUDA(cudaStreamSynchronize(st));
+  out->overflow = (int64_t)hnf;
+
+  // final elite train semantics: slot rec_slot[g]; a parent-sourced elite
+  // lives in the elite buffer selected by the final parity (gsm.cu)
+  const int64_t slot = out->elite_slot[g];
+  const bool redirected = (g > 0 && hctl[CTL_REDIRECT] == slot);
+  for (auto& p : sh) {
+    if (p->ntr == 0 || !out->elite_train_semantics) continue;
+    const char* src = redirected ? (const char*)p->elite[hctl[CTL_PARITY] & 1].p
+                                 : (const char*)p->S.p + slot * p->pitch * esz;
+    double* dst = out->elite_train_semantics + p->tr_lo;
+    if (f64) {
+      GSGP_CUDA(cudaMemcpy(dst, src, p->ntr * 8, cudaMemcpyDeviceToHost));
+    } else {
+      std::vector<float> tmp(p->ntr);
+      GSGP_CUDA(cudaMemcpy(tmp.data(), src, p->ntr * 4, cudaMemcpyDeviceToHost));
+      for (int64_t j = 0; j < p->ntr; ++j) dst[j] = (double)tmp[j];
+    }
+  }
+
+  auto t_host1 = std::chrono::steady_clock::now();
+  const double evo = elapsed_ms(ev_loop0, ev_loop1);
+  out->stage_ms[0] = elapsed_ms(ev_begin, ev_created);
+  out->stage_ms[1] = elapsed_ms(ev_created, ev_sem);
+  out->stage_ms[2] = evo;
+  out->stage_ms[3] = g > 0 ? evo / (double)g : 0.0;
+  out->stage_ms[4] = std::chrono::duration<double, std::milli>(t_host1 - t_host0).count();
+  out->stage_ms[5] = gsm_ms;
+  int64_t gsm_per_gen = 0;
+  for (auto& p : sh) gsm_per_gen += p->pitch > 0 ? 1 : 0;
+  out->stage_ms[6] = timed ? (double)(g * gsm_per_gen) : 0.0;
+  out->stage_ms[7] = (double)(g * launches_per_gen);
+  out->stage_ms[8] = elapsed_ms(ev_win0, ev_loop1);
+  out->stage_ms[9] = win_gsm_ms;
+  out->stage_ms[10] = timed ? (double)((g - w0) * gsm_per_gen) : 0.0;
+  out->stage_ms[11] = (double)((g - w0) * launches_per_gen);
+}
+
+}  // namespace gsgp

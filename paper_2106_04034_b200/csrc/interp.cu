@@ -1,0 +1,340 @@
+// ComputeSemantics on sm_100a: genome compile + case-parallel fp64 interpreter.
+//
+// Reference semantics (gsgp/interpreter.py:45-119): postfix scan with a LIFO
+// stack; a function fires only when two operands are stacked (else it is
+// skipped), left operand = second pop, protected division gives 1.0 when
+// |den| < eps, and the program value is the last fired result, else the
+// stack top, else 0.0.  Whether a gene fires depends only on the tag
+// sequence (interpreter.py:10-15), so each genome is compiled ONCE into the
+// expression tree rooted at its output node:
+//   * skipped genes and every gene outside that tree are dropped (dead code);
+//   * subtrees without a feature are folded to a constant with the same
+//     fp64 operations (bit-identical: each node is a pure IEEE function of
+//     its children);
+//   * children are evaluated in Sethi-Ullman order with terminal operands
+//     folded into the instruction, so the spill stack is <= log2(nodes)+1.
+// The evaluator then runs one thread per fitness case (CPT cases per thread
+// for ILP) over a block-uniform instruction stream — every branch is
+// warp-uniform — with the block's feature tile and spill stacks in shared
+// memory.
+#include "kernels.cuh"
+
+namespace gsgp {
+
+namespace {
+
+constexpr uint8_t F_EXISTS = 0x80, F_CONST = 0x40, F_FEAT = 0x20, F_NEED = 0x1f;
+
+__device__ __forceinline__ bool is_leaf(uint8_t f) { return (f & (F_CONST | F_FEAT)) != 0; }
+
+// one thread per genome; scratch is per-genome global memory
+__global__ void k_compile(const uint8_t* __restrict__ tags, const int32_t* __restrict__ codes,
+                          const double* __restrict__ consts, int64_t count, int32_t k, double eps,
+                          Program P) {
+  int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= count) return;
+  const uint8_t* T = tags + g * k;
+  const int32_t* C = codes + g * k;
+  const double* V = consts + g * k;
+  int32_t* stk = P.scratch + g * 4 * (int64_t)k;
+  int32_t* Lc = stk + k;
+  int32_t* Rc = Lc + k;
+  int32_t* work = Rc + k;
+  uint8_t* fl = P.flags + g * (int64_t)k;
+  double* cv = P.cval + g * (int64_t)k;
+  Ins* out = P.code + g * (int64_t)(k + 1);
+
+  // ---- structural scan (interpreter.py:53-70) with attributes in postfix order
+  int32_t sp = 0, last = -1;
+  for (int32_t j = 0; j < k; ++j) {
+    uint8_t t = T[j];
+    if (t == TAG_FUNCTION) {
+      if (sp < 2) { fl[j] = 0; continue; }          // skipped: operands unavailable
+      int32_t r = stk[--sp], l = stk[--sp];
+      Lc[j] = l; Rc[j] = r;
+      stk[sp++] = j;
+      last = j;
+      uint8_t fa = fl[l], fb = fl[r];
+      if ((fa & F_CONST) && (fb & F_CONST)) {
+        cv[j] = apply_op(C[j], cv[l], cv[r], eps);   // constant folding, same IEEE op
+        fl[j] = F_EXISTS | F_CONST;
+      } else {
+        bool la = is_leaf(fa), lb = is_leaf(fb);
+        int na = la ? 0 : (fa & F_NEED), nb = lb ? 0 : (fb & F_NEED);
+        int need;
+        if (la && lb) need = 0;
+        else if (lb) need = na;
+        else if (la) need = nb;
+        else need = (na == nb) ? na + 1 : (na > nb ? na : nb);
+        fl[j] = F_EXISTS | (uint8_t)need;
+      }
+    } else if (t == TAG_FEATURE) {
+      fl[j] = F_EXISTS | F_FEAT;
+      stk[sp++] = j;
+    } else {
+      fl[j] = F_EXISTS | F_CONST;
+      cv[j] = V[j];
+      stk[sp++] = j;
+    }
+  }
+  int32_t root = last >= 0 ? last : (sp > 0 ? stk[sp - 1] : -1);
+
+  auto leaf_src = [&](int32_t n, uint8_t& src, uint16_t& f, double& c) {
+    if (fl[n] & F_CONST) { src = SRC_CONST; c = cv[n]; }
+    else { src = SRC_FEAT; f = (uint16_t)C[n]; }
+  };
+
+  int32_t pc = 0;
+  int depth = 0;
+  if (root < 0 || is_leaf(fl[root])) {
+    Ins in{};
+    in.op = INS_LOAD;
+    if (root < 0) { in.ls = SRC_CONST; in.c = 0.0; }
+    else leaf_src(root, in.ls, in.lf, in.c);
+    out[pc++] = in;
+  } else {
+    depth = fl[root] & F_NEED;
+    // ---- iterative Sethi-Ullman emission; frame = node*4 + state
+    int32_t top = 0;
+    work[top++] = root * 4;
+    while (top > 0) {
+      int32_t fr = work[top - 1];
+      int32_t n = fr >> 2, st = fr & 3;
+      int32_t l = Lc[n], r = Rc[n];
+      bool la = is_leaf(fl[l]), lb = is_leaf(fl[r]);
+      bool both = !la && !lb;
+      bool left_first = both ? ((fl[l] & F_NEED) >= (fl[r] & F_NEED)) : !la;
+      int32_t first = left_first ? l : r, second = left_first ? r : l;
+      if (st == 0 && !(la && lb)) {
+        work[top - 1] = n * 4 + 1;
+        work[top++] = first * 4;
+        continue;
+      }
+      if (st == 1 && both) {
+        Ins p{};
+        p.op = INS_PUSH;
+        out[pc++] = p;
+        work[top - 1] = n * 4 + 2;
+        work[top++] = second * 4;
+        continue;
+      }
+      Ins in{};
+      in.op = (uint8_t)C[n];
+      if (la && lb) {
+        leaf_src(l, in.ls, in.lf, in.c);
+        leaf_src(r, in.rs, in.rf, in.c);
+      } else if (both) {
+        in.ls = left_first ? SRC_POP : SRC_ACC;
+        in.rs = left_first ? SRC_ACC : SRC_POP;
+      } else if (lb) {                 // right operand is a terminal
+        in.ls = SRC_ACC;
+        leaf_src(r, in.rs, in.rf, in.c);
+      } else {                         // left operand is a terminal
+        leaf_src(l, in.ls, in.lf, in.c);
+        in.rs = SRC_ACC;
+      }
+      out[pc++] = in;
+      --top;
+    }
+  }
+  P.len[g] = pc;
+  P.depth[g] = depth;
+  atomicMax(P.maxdepth, depth);
+}
+
+template <int CPT, int MODE, typename TOut, bool kXSmem>
+__global__ void __launch_bounds__(128) k_interpret(InterpArgs a, int64_t ntiles, int64_t gpb) {
+  constexpr int B = 128;
+  constexpr int TILE = B * CPT;
+  extern __shared__ double smem[];
+  const int tid = threadIdx.x;
+  const int64_t tile = blockIdx.x;
+  const int64_t q0 = tile * TILE;
+  const int64_t N = a.ntr + a.nte;
+  double* xs = smem;                                  // [l][TILE] when kXSmem
+  double* stack = smem + (kXSmem ? (int64_t)a.l * TILE : 0);   // [maxdepth][TILE]
+  __shared__ double red[32];
+
+  if (kXSmem) {
+    for (int64_t e = tid; e < (int64_t)a.l * TILE; e += B) {
+      int64_t f = e / TILE, c = e - f * TILE;
+      int64_t q = q0 + c;
+      xs[e] = q < N ? a.XT[f * a.xt_pitch + q] : 0.0;
+    }
+    __syncthreads();
+  }
+  double ytr[CPT];
+  int64_t col[CPT];
+  bool valid[CPT], train[CPT];
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) {
+    int64_t q = q0 + c * B + tid;
+    valid[c] = q < N;
+    train[c] = q < a.ntr;
+    col[c] = train[c] ? q : a.test_off + (q - a.ntr);
+    ytr[c] = (MODE == INTERP_POP && valid[c]) ? a.y[q] : 0.0;
+  }
+  unsigned long long nonfinite = 0;
+
+  const int64_t g0 = blockIdx.y * gpb;
+  const int64_t g1 = min(a.count, g0 + gpb);
+  for (int64_t g = g0; g < g1; ++g) {
+    const uint4* code = reinterpret_cast<const uint4*>(a.code + g * a.k1);
+    const int len = a.len[g];
+    double acc[CPT];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) acc[c] = 0.0;
+    int sp = 0;
+    for (int i = 0; i < len; ++i) {
+      uint4 raw = __ldg(code + i);
+      const int op = raw.x & 0xff, ls = (raw.x >> 8) & 0xff, rs = (raw.x >> 16) & 0xff;
+      const int lf = raw.y & 0xffff, rf = raw.y >> 16;
+      const double cst = __hiloint2double((int)raw.w, (int)raw.z);
+      if (op == INS_PUSH) {
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) stack[(int64_t)sp * TILE + c * B + tid] = acc[c];
+        ++sp;
+        continue;
+      }
+      if (ls == SRC_POP || rs == SRC_POP) --sp;
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) {
+        const int64_t cc = c * B + tid;
+        double lv, rv;
+        switch (ls) {
+          case SRC_ACC: lv = acc[c]; break;
+          case SRC_POP: lv = stack[(int64_t)sp * TILE + cc]; break;
+          case SRC_FEAT: lv = kXSmem ? xs[(int64_t)lf * TILE + cc]
+                                     : (valid[c] ? a.XT[lf * a.xt_pitch + q0 + cc] : 0.0); break;
+          default: lv = cst;
+        }
+        if (op == INS_LOAD) { acc[c] = lv; continue; }
+        switch (rs) {
+          case SRC_ACC: rv = acc[c]; break;
+          case SRC_POP: rv = stack[(int64_t)sp * TILE + cc]; break;
+          case SRC_FEAT: rv = kXSmem ? xs[(int64_t)rf * TILE + cc]
+                                     : (valid[c] ? a.XT[rf * a.xt_pitch + q0 + cc] : 0.0); break;
+          default: rv = cst;
+        }
+        acc[c] = apply_op(op, lv, rv, a.eps);
+      }
+    }
+    // ---- epilogue: non-finite -> 0.0 counted (core.py:348-356), then store
+    double sse_tr = 0.0, sse_te = 0.0;
+    int wide = 0;
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      if (!valid[c]) continue;
+      double v = acc[c];
+      if (!isfinite(v) && !(MODE == INTERP_F64 && a.raw)) { v = 0.0; ++nonfinite; }
+      const int64_t q = q0 + c * B + tid;
+      if (MODE == INTERP_F64) {
+        a.out64[g * N + q] = v;
+      } else if (MODE == INTERP_POP) {
+        TOut o = (TOut)v;
+        reinterpret_cast<TOut*>(a.out)[g * a.pitch + col[c]] = o;
+        if (isinf((double)o)) wide |= train[c] ? 1 : 2;
+        double d = __dsub_rn(v, ytr[c]);
+        if (train[c]) sse_tr = __dadd_rn(sse_tr, __dmul_rn(d, d));
+        else sse_te = __dadd_rn(sse_te, __dmul_rn(d, d));
+      } else {
+        // sigmoid of the pool, once per run (mutation.py:32-34, evolution.py:135-136)
+        double sg = __ddiv_rn(1.0, __dadd_rn(1.0, exp(-v)));
+        reinterpret_cast<TOut*>(a.out)[g * a.pitch + col[c]] = (TOut)sg;
+      }
+    }
+    if (MODE == INTERP_POP) {
+      // fixed-order block reduction of the tile's SSE (train, test)
+      sse_tr = warp_sum(sse_tr);
+      sse_te = warp_sum(sse_te);
+      int wb = __reduce_or_sync(0xffffffffu, wide);
+      if ((tid & 31) == 0) {
+        red[(tid >> 5) * 2] = sse_tr;
+        red[(tid >> 5) * 2 + 1] = sse_te;
+        if (wb) atomicOr(a.wide + g, wb);
+      }
+      __syncthreads();
+      if (tid < 2) {
+        double t = 0.0;
+        for (int w = 0; w < B / 32; ++w) t = __dadd_rn(t, red[w * 2 + tid]);
+        a.part[(g * ntiles + tile) * 2 + tid] = t;
+      }
+      __syncthreads();
+    }
+  }
+  // block total of replaced elements (integer: order-independent)
+  for (int o = 16; o > 0; o >>= 1) nonfinite += __shfl_xor_sync(0xffffffffu, nonfinite, o);
+  if ((tid & 31) == 0 && nonfinite) atomicAdd(a.nonfinite, nonfinite);
+}
+
+int choose_cpt(int l) { return l <= 16 ? 4 : (l <= 48 ? 2 : 1); }
+
+template <int CPT, int MODE, typename TOut>
+void launch_cpt(const InterpArgs& a, cudaStream_t s) {
+  constexpr int TILE = 128 * CPT;
+  const int64_t N = a.ntr + a.nte;
+  const int64_t ntiles = (N + TILE - 1) / TILE;
+  const size_t stack_bytes = (size_t)(a.maxdepth > 0 ? a.maxdepth : 1) * TILE * sizeof(double);
+  const size_t x_bytes = (size_t)a.l * TILE * sizeof(double);
+  const bool xsmem = x_bytes + stack_bytes <= 160 * 1024;
+  const size_t smem = (xsmem ? x_bytes : 0) + stack_bytes;
+  GSGP_REQUIRE(smem <= 200 * 1024, "interpreter spill stack too deep for shared memory");
+  // genomes per block: enough blocks to fill 148 SMs several times over
+  int64_t want = 148 * 8;
+  int64_t gpb = (a.count * ntiles + want - 1) / want;
+  if (gpb < 1) gpb = 1;
+  if (gpb > 64) gpb = 64;
+  int64_t gy = (a.count + gpb - 1) / gpb;
+  GSGP_REQUIRE(gy <= 65535, "too many genome groups");
+  dim3 grid((unsigned)ntiles, (unsigned)gy);
+  if (xsmem) {
+    auto k = k_interpret<CPT, MODE, TOut, true>;
+    GSGP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<grid, 128, smem, s>>>(a, ntiles, gpb);
+  } else {
+    auto k = k_interpret<CPT, MODE, TOut, false>;
+    GSGP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<grid, 128, smem, s>>>(a, ntiles, gpb);
+  }
+  GSGP_CUDA(cudaGetLastError());
+}
+
+template <int MODE, typename TOut>
+void launch_mode(const InterpArgs& a, cudaStream_t s) {
+  switch (choose_cpt(a.l)) {
+    case 4: launch_cpt<4, MODE, TOut>(a, s); break;
+    case 2: launch_cpt<2, MODE, TOut>(a, s); break;
+    default: launch_cpt<1, MODE, TOut>(a, s); break;
+  }
+}
+
+}  // namespace
+
+void launch_compile(const uint8_t* tags, const int32_t* codes, const double* consts, int64_t count,
+                    int32_t k, double eps, Program prog, cudaStream_t s) {
+  if (count <= 0) return;
+  GSGP_CUDA(cudaMemsetAsync(prog.maxdepth, 0, sizeof(int32_t), s));
+  k_compile<<<(unsigned)((count + 63) / 64), 64, 0, s>>>(tags, codes, consts, count, k, eps, prog);
+  GSGP_CUDA(cudaGetLastError());
+}
+
+int64_t interp_tiles(const InterpArgs& a, int* cpt_out) {
+  int cpt = choose_cpt(a.l);
+  if (cpt_out) *cpt_out = cpt;
+  int64_t tile = 128 * cpt;
+  return (a.ntr + a.nte + tile - 1) / tile;
+}
+
+void launch_interpret(const InterpArgs& a, int mode, cudaStream_t s) {
+  if (a.count <= 0 || a.ntr + a.nte <= 0) return;
+  if (mode == INTERP_F64) launch_mode<INTERP_F64, double>(a, s);
+  else if (mode == INTERP_POP) {
+    if (a.out_is_f64) launch_mode<INTERP_POP, double>(a, s);
+    else launch_mode<INTERP_POP, float>(a, s);
+  } else {
+    if (a.out_is_f64) launch_mode<INTERP_POOL, double>(a, s);
+    else launch_mode<INTERP_POOL, float>(a, s);
+  }
+}
+
+}  // namespace gsgp

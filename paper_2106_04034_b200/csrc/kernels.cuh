@@ -1,0 +1,134 @@
+// Launchers for the sm_100a kernels.  All launchers are asynchronous on the
+// given stream and throw gsgp::Error on launch failure.
+#pragma once
+
+#include "common.cuh"
+
+namespace gsgp {
+
+// ------------------------------------------------------------ rng / genomes
+void launch_rng_draw(uint64_t seed, uint64_t stream, const uint64_t* counters, int64_t n,
+                     uint64_t* bits, double* units, cudaStream_t s);
+
+struct GeneParams {
+  uint64_t seed;
+  double thr_fun;        // p_fun
+  double thr_feat;       // p_fun + p_feat
+  double erc_low, erc_high;
+  int32_t n_features;
+  int32_t k;
+};
+// gene (i, j) of streams [stream_base, stream_base + count)
+void launch_create_population(const GeneParams& p, int64_t count, uint64_t stream_base,
+                              uint8_t* tags, int32_t* codes, double* consts, cudaStream_t s);
+
+// ------------------------------------------------------------ plan
+struct PlanParams {
+  uint64_t seed;
+  int64_t m, r;
+  int32_t ms_uniform;
+  double ms_const;
+};
+// plan for generation `gen` (explicit) or, when gen_ptr != nullptr, for
+// generation *gen_ptr read on device (graph-replayable)
+void launch_plan(const PlanParams& p, int64_t gen, const int64_t* gen_ptr, int64_t* u, int64_t* v,
+                 double* ms, int64_t stride_per_gen, cudaStream_t s);
+
+// ------------------------------------------------------------ compile + interpret
+struct Program {
+  Ins* code;            // [count][k+1]
+  int32_t* len;         // [count]
+  int32_t* depth;       // [count] spill-stack depth
+  int32_t* maxdepth;    // [1] max over genomes (atomicMax)
+  int32_t* scratch;     // [count][4*k] ints
+  uint8_t* flags;       // [count][k]
+  double* cval;         // [count][k]
+};
+void launch_compile(const uint8_t* tags, const int32_t* codes, const double* consts, int64_t count,
+                    int32_t k, double eps, Program prog, cudaStream_t s);
+
+enum InterpMode : int { INTERP_F64 = 0, INTERP_POP = 1, INTERP_POOL = 2 };
+
+struct InterpArgs {
+  const Ins* code;
+  const int32_t* len;
+  int64_t k1;               // instruction stride per genome (k + 1)
+  int64_t count;            // genomes
+  const double* XT;         // [l][ncase_pitch] fp64, feature-major, cases stacked train|test
+  int64_t xt_pitch;
+  int32_t l;
+  int64_t ntr, nte;         // local case counts (stacked index q < ntr is train)
+  double eps;
+  int32_t maxdepth;
+  // outputs
+  double* out64;            // INTERP_F64: [count][ntr+nte]
+  void* out;                // INTERP_POP/POOL: [count][pitch] float or double
+  int32_t out_is_f64;
+  int64_t pitch;            // storage pitch (elements); test region starts at test_off
+  int64_t test_off;
+  const double* y;          // [ntr+nte] stacked targets (INTERP_POP)
+  double* part;             // [count][ntiles][2] SSE partials (INTERP_POP)
+  int32_t* wide;            // [count] bit0 train overflowed fp32, bit1 test (INTERP_POP)
+  unsigned long long* nonfinite;   // element count replaced by 0.0
+  int32_t raw;              // INTERP_F64 only: keep non-finite values (scalar interpret)
+};
+int64_t interp_tiles(const InterpArgs& a, int* cpt_out);
+void launch_interpret(const InterpArgs& a, int mode, cudaStream_t s);
+
+// ------------------------------------------------------------ generation
+struct GsmArgs {
+  const void* pool;         // [r][pitch] squashed trees (float or double)
+  void* S;                  // [m][pitch] semantics, updated in place
+  const void* elite_prev;   // [pitch] saved parent elite row (redirect target)
+  void* elite_cur;          // [pitch] parent row b_p is saved here
+  const double* y;          // [pitch] targets in storage layout (0 in padding)
+  int64_t pitch, test_off;
+  int64_t m;
+  const int64_t* u;         // plan of this generation (or base when gen_ptr != nullptr)
+  const int64_t* v;
+  const double* ms;
+  const int64_t* ctl;       // device control block (see engine.cu), may be nullptr
+  int32_t sign;             // 0 minus, 1 plus
+  double* part;             // [m][ntiles][2]
+  unsigned long long* nonfinite;   // operator mode only
+};
+int64_t gsm_tiles(int64_t pitch, bool f64);
+void launch_gsm(const GsmArgs& a, bool f64, bool operator_mode, cudaStream_t s);
+
+// sum [rows][ntiles][2] partials (fixed order) into out[rows][2] (+= when accumulate)
+void launch_reduce_partials(const double* part, int64_t rows, int64_t ntiles, double* out,
+                            bool accumulate, cudaStream_t s);
+// out[i] = sum_s in[s][i] for s in shard order
+void launch_sum_shards(const double* const* in, int nshards, int64_t n, double* out, cudaStream_t s);
+
+// fp64 operator RMSE per row of a dense [m][n] matrix (fitness.py:28-51)
+void launch_row_rmse(const double* S, const double* y, int64_t m, int64_t n, double* out,
+                     cudaStream_t s);
+
+struct SurviveArgs {
+  int64_t m;
+  double ntr, nte;
+  const double* sse_off;    // [m][2] offspring SSE (train, test), already exchanged
+  double* F;                // [m] state train fitness (in: parent, out: next)
+  double* TS;               // [m] state test SSE
+  int32_t* wide;            // [m] slot flags
+  double* Fo;               // [m] scratch
+  double* To;               // [m] scratch
+  int64_t* ctl;             // control block
+  // lineage record for this generation (index = ctl[CTL_GEN])
+  int8_t* rec_src; int64_t* rec_idx; int64_t* rec_slot; double* rec_fit;
+  double* trace_tr; double* trace_te;
+};
+void launch_survive(const SurviveArgs& a, cudaStream_t s);
+// initial elite: fitness from SSE, argmin, trace[0] (evolution.py:132-143)
+void launch_init_state(const SurviveArgs& a, cudaStream_t s);
+// decision only, for the operator API: out = {src, idx, slot}
+void launch_survive_decision(const double* fp, const double* fo, int64_t m, int64_t* out,
+                             cudaStream_t s);
+
+// np.argmin / np.argmax of a vector: out = {argmin, argmax}
+void launch_argminmax(const double* f, int64_t m, int64_t* out, cudaStream_t s);
+// elementwise fp64 sigmoid (mutation.py:32-34)
+void launch_sigmoid(const double* x, int64_t n, double* y, cudaStream_t s);
+
+}  // namespace gsgp

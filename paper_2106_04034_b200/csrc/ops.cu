@@ -1,0 +1,385 @@
+// Small kernels of the hot path: counter RNG, CreatePopulation, mutation plan,
+// deterministic reductions, RMSE and elitist survival.
+//
+// Reference citations: gsgp/X.py:N means /root/reference/pkg/src/gsgp/X.py:N.
+#include "kernels.cuh"
+
+namespace gsgp {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+inline unsigned blocks_for(int64_t n, int threads = kThreads) {
+  int64_t b = (n + threads - 1) / threads;
+  return (unsigned)(b < 1 ? 1 : b);
+}
+
+inline void check_launch() { GSGP_CUDA(cudaGetLastError()); }
+
+// ---------------------------------------------------------------- rng
+__global__ void k_rng_draw(uint64_t key, const uint64_t* __restrict__ counters, int64_t n,
+                           uint64_t* bits, double* units) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint64_t b = draw_bits(key, counters[i]);
+  if (bits) bits[i] = b;
+  if (units) units[i] = (double)(b >> 11) * 0x1p-53;
+}
+
+// --------------------------------------------------- CreatePopulation
+// gsgp/population.py:47-70: gene (i, j) uses stream base+i, counter 2j for the
+// tag and 2j+1 for the payload; non-owning fields are zero.
+__global__ void k_create_population(GeneParams p, int64_t count, uint64_t stream_base,
+                                    uint8_t* __restrict__ tags, int32_t* __restrict__ codes,
+                                    double* __restrict__ consts) {
+  int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (gid >= count * (int64_t)p.k) return;
+  int64_t i = gid / p.k;
+  uint64_t j = (uint64_t)(gid - i * p.k);
+  uint64_t key = stream_key(p.seed, stream_base + (uint64_t)i);
+  double d_tag = draw_unit(key, 2 * j);
+  double d_pay = draw_unit(key, 2 * j + 1);
+  uint8_t tag;
+  int32_t code = 0;
+  double c = 0.0;
+  if (d_tag < p.thr_fun) {
+    tag = TAG_FUNCTION;
+    int32_t op = (int32_t)__dmul_rn(d_pay, 4.0);          // population.py:64
+    code = op < 3 ? op : 3;
+  } else if (d_tag < p.thr_feat) {
+    tag = TAG_FEATURE;
+    int32_t f = (int32_t)__dmul_rn(d_pay, (double)p.n_features);   // population.py:65
+    code = f < p.n_features - 1 ? f : p.n_features - 1;
+  } else {
+    tag = TAG_CONSTANT;                                    // population.py:70
+    c = __dadd_rn(p.erc_low, __dmul_rn(d_pay, __dsub_rn(p.erc_high, p.erc_low)));
+  }
+  tags[gid] = tag;
+  codes[gid] = code;
+  consts[gid] = c;
+}
+
+// ---------------------------------------------------------------- plan
+// gsgp/mutation.py:37-62: stream 2^32 + gen, slot i draws counters 3i, 3i+1,
+// 3i+2; u uniform over [0, r), v uniform over the other r-1 indices.
+__global__ void k_plan(PlanParams p, int64_t gen, const int64_t* gen_ptr, int64_t* u, int64_t* v,
+                       double* ms, int64_t stride) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= p.m) return;
+  int64_t g = gen_ptr ? gen_ptr[CTL_GEN] : gen;
+  int64_t off = gen_ptr ? (g - 1) * stride : 0;
+  uint64_t key = stream_key(p.seed, kPlanStream0 + (uint64_t)g);
+  uint64_t c = 3ull * (uint64_t)i;
+  double du = draw_unit(key, c), dv = draw_unit(key, c + 1);
+  int64_t a = (int64_t)__dmul_rn(du, (double)p.r);
+  a = a < p.r - 1 ? a : p.r - 1;
+  int64_t b = (int64_t)__dmul_rn(dv, (double)(p.r - 1));
+  b = b < p.r - 2 ? b : p.r - 2;
+  b += (b >= a);
+  u[off + i] = a;
+  v[off + i] = b;
+  ms[off + i] = p.ms_uniform ? __dsub_rn(1.0, draw_unit(key, c + 2)) : p.ms_const;
+}
+
+// ------------------------------------------------------- reductions
+// Block-wide fp64 sum with a fixed order: per-warp butterfly, then warps in
+// index order.  Every thread gets the result.
+__device__ double block_sum(double v, double* sh) {
+  v = warp_sum(v);
+  int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  int nw = blockDim.x >> 5;
+  for (int i = 0; i < nw; ++i) t = __dadd_rn(t, sh[i]);
+  return t;
+}
+
+// part[row][tile][2] -> out[row][2]; tiles are summed per thread in index
+// order, then combined by a fixed tree: a function of case positions only.
+__global__ void k_reduce_partials(const double* __restrict__ part, int64_t ntiles,
+                                  double* __restrict__ out, int accumulate) {
+  __shared__ double sh[32];
+  int64_t row = blockIdx.x;
+  const double* p = part + row * ntiles * 2;
+  double a = 0.0, b = 0.0;
+  for (int64_t t = threadIdx.x; t < ntiles; t += blockDim.x) {
+    a = __dadd_rn(a, p[2 * t]);
+    b = __dadd_rn(b, p[2 * t + 1]);
+  }
+  a = block_sum(a, sh);
+  b = block_sum(b, sh);
+  if (threadIdx.x == 0) {
+    if (accumulate) {
+      out[2 * row] = __dadd_rn(out[2 * row], a);
+      out[2 * row + 1] = __dadd_rn(out[2 * row + 1], b);
+    } else {
+      out[2 * row] = a;
+      out[2 * row + 1] = b;
+    }
+  }
+}
+
+struct ShardPtrs {
+  const double* p[16];
+};
+
+__global__ void k_sum_shards(ShardPtrs in, int nshards, int64_t n, double* out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double t = in.p[0][i];
+  for (int s = 1; s < nshards; ++s) t = __dadd_rn(t, in.p[s][i]);
+  out[i] = t;
+}
+
+// fp64 RMSE of each row (operator API, fitness.py:28-51)
+__global__ void k_row_rmse(const double* __restrict__ S, const double* __restrict__ y, int64_t n,
+                           double* out) {
+  __shared__ double sh[32];
+  const double* row = S + blockIdx.x * n;
+  double a = 0.0;
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+    double d = __dsub_rn(row[j], y[j]);
+    a = __dadd_rn(a, __dmul_rn(d, d));
+  }
+  a = block_sum(a, sh);
+  if (threadIdx.x == 0) out[blockIdx.x] = rmse_of(a, (double)n);
+}
+
+// ---------------------------------------------------------- arg-min/max
+// np.argmin / np.argmax semantics: ties go to the lowest index
+// (gsgp/evolution.py:36-47).  Values are never NaN (fitness.py:25 maps
+// non-finite RMSE to +inf).
+struct ArgVal {
+  double v;
+  int64_t i;
+};
+
+__device__ __forceinline__ ArgVal better_min(ArgVal a, ArgVal b) {
+  if (b.v < a.v || (b.v == a.v && b.i < a.i)) return b;
+  return a;
+}
+__device__ __forceinline__ ArgVal better_max(ArgVal a, ArgVal b) {
+  if (b.v > a.v || (b.v == a.v && b.i < a.i)) return b;
+  return a;
+}
+
+template <bool kMin>
+__device__ ArgVal block_arg(ArgVal x, ArgVal* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ArgVal y{__shfl_xor_sync(0xffffffffu, x.v, o), __shfl_xor_sync(0xffffffffu, x.i, o)};
+    x = kMin ? better_min(x, y) : better_max(x, y);
+  }
+  int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) sh[w] = x;
+  __syncthreads();
+  ArgVal r = sh[0];
+  for (int i = 1; i < (int)(blockDim.x >> 5); ++i) r = kMin ? better_min(r, sh[i]) : better_max(r, sh[i]);
+  return r;
+}
+
+constexpr ArgVal kMinInit{INFINITY, INT64_MAX};
+constexpr ArgVal kMaxInit{-INFINITY, INT64_MAX};
+
+// ------------------------------------------------------------- survival
+// gsgp/evolution.py:65-83 plus the loop bookkeeping at :146-158.
+// Slot flags (wide): a slot whose semantics overflowed fp32 at
+// initialisation keeps its (constant) fp64 fitness — see DESIGN.md §4.
+__global__ void k_survive(SurviveArgs a) {
+  __shared__ ArgVal sh[32];
+  __shared__ int64_t dec[4];
+  const int64_t m = a.m;
+  ArgVal bp = kMinInit, bo = kMinInit, wo = kMaxInit;
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+    int32_t fl = a.wide[i];
+    double fo = (fl & 1) ? a.F[i] : rmse_of(a.sse_off[2 * i], a.ntr);
+    double to = (fl & 2) ? a.TS[i] : a.sse_off[2 * i + 1];
+    a.Fo[i] = fo;
+    a.To[i] = to;
+    bp = better_min(bp, ArgVal{a.F[i], i});
+    bo = better_min(bo, ArgVal{fo, i});
+    wo = better_max(wo, ArgVal{fo, i});
+  }
+  bp = block_arg<true>(bp, sh);
+  bo = block_arg<true>(bo, sh);
+  wo = block_arg<false>(wo, sh);
+  if (threadIdx.x == 0) {
+    int64_t g = a.ctl[CTL_GEN];
+    int8_t src;
+    int64_t idx, slot;
+    double fit;
+    if (bp.v < bo.v) {                       // strict: exact ties keep the offspring
+      src = 0; idx = bp.i; slot = wo.i; fit = bp.v;
+      int32_t fl = a.wide[idx];
+      double ts = a.TS[idx];
+      a.Fo[slot] = fit;
+      a.To[slot] = ts;
+      a.wide[slot] = fl;
+      a.ctl[CTL_REDIRECT] = slot;
+      a.ctl[CTL_PARENT_ELITES] += 1;
+    } else {
+      src = 1; idx = bo.i; slot = bo.i; fit = bo.v;
+      a.ctl[CTL_REDIRECT] = -1;
+    }
+    a.rec_src[g] = src;
+    a.rec_idx[g] = idx;
+    a.rec_slot[g] = slot;
+    a.rec_fit[g] = fit;
+    a.trace_tr[g] = fit;
+    a.trace_te[g] = rmse_of(a.To[slot], a.nte);
+    dec[0] = slot;
+  }
+  __syncthreads();
+  ArgVal nb = kMinInit;
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+    double f = a.Fo[i];
+    a.F[i] = f;
+    a.TS[i] = a.To[i];
+    nb = better_min(nb, ArgVal{f, i});
+  }
+  nb = block_arg<true>(nb, sh);
+  if (threadIdx.x == 0) {
+    a.ctl[CTL_BP] = nb.i;
+    a.ctl[CTL_PARITY] ^= 1;
+    a.ctl[CTL_GEN] += 1;
+  }
+}
+
+// evolution.py:132-143: initial fitness, elite and trace[0]
+__global__ void k_init_state(SurviveArgs a) {
+  __shared__ ArgVal sh[32];
+  ArgVal b = kMinInit;
+  for (int64_t i = threadIdx.x; i < a.m; i += blockDim.x) {
+    double f = rmse_of(a.sse_off[2 * i], a.ntr);
+    a.F[i] = f;
+    a.TS[i] = a.sse_off[2 * i + 1];
+    b = better_min(b, ArgVal{f, i});
+  }
+  b = block_arg<true>(b, sh);
+  if (threadIdx.x == 0) {
+    a.rec_src[0] = 2;   // "initial"
+    a.rec_idx[0] = b.i;
+    a.rec_slot[0] = b.i;
+    a.rec_fit[0] = b.v;
+    a.trace_tr[0] = b.v;
+    a.trace_te[0] = rmse_of(a.sse_off[2 * b.i + 1], a.nte);
+    a.ctl[CTL_GEN] = 1;
+    a.ctl[CTL_BP] = b.i;
+    a.ctl[CTL_REDIRECT] = -1;
+    a.ctl[CTL_PARITY] = 0;
+    a.ctl[CTL_PARENT_ELITES] = 0;
+  }
+}
+
+__global__ void k_survive_decision(const double* fp, const double* fo, int64_t m, int64_t* out) {
+  __shared__ ArgVal sh[32];
+  ArgVal bp = kMinInit, bo = kMinInit, wo = kMaxInit;
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+    bp = better_min(bp, ArgVal{fp[i], i});
+    bo = better_min(bo, ArgVal{fo[i], i});
+    wo = better_max(wo, ArgVal{fo[i], i});
+  }
+  bp = block_arg<true>(bp, sh);
+  bo = block_arg<true>(bo, sh);
+  wo = block_arg<false>(wo, sh);
+  if (threadIdx.x == 0) {
+    if (bp.v < bo.v) { out[0] = 0; out[1] = bp.i; out[2] = wo.i; }
+    else { out[0] = 1; out[1] = bo.i; out[2] = bo.i; }
+  }
+}
+
+__global__ void k_argminmax(const double* f, int64_t m, int64_t* out) {
+  __shared__ ArgVal sh[32];
+  ArgVal lo = kMinInit, hi = kMaxInit;
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+    lo = better_min(lo, ArgVal{f[i], i});
+    hi = better_max(hi, ArgVal{f[i], i});
+  }
+  lo = block_arg<true>(lo, sh);
+  hi = block_arg<false>(hi, sh);
+  if (threadIdx.x == 0) { out[0] = lo.i; out[1] = hi.i; }
+}
+
+__global__ void k_sigmoid_vec(const double* x, int64_t n, double* y) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) y[i] = __ddiv_rn(1.0, __dadd_rn(1.0, exp(-x[i])));   // mutation.py:32-34
+}
+
+}  // namespace
+
+// ------------------------------------------------------------- launchers
+void launch_argminmax(const double* f, int64_t m, int64_t* out, cudaStream_t s) {
+  k_argminmax<<<1, 1024, 0, s>>>(f, m, out);
+  check_launch();
+}
+
+void launch_sigmoid(const double* x, int64_t n, double* y, cudaStream_t s) {
+  if (n <= 0) return;
+  k_sigmoid_vec<<<blocks_for(n), kThreads, 0, s>>>(x, n, y);
+  check_launch();
+}
+
+void launch_rng_draw(uint64_t seed, uint64_t stream, const uint64_t* counters, int64_t n,
+                     uint64_t* bits, double* units, cudaStream_t s) {
+  if (n <= 0) return;
+  k_rng_draw<<<blocks_for(n), kThreads, 0, s>>>(stream_key(seed, stream), counters, n, bits, units);
+  check_launch();
+}
+
+void launch_create_population(const GeneParams& p, int64_t count, uint64_t stream_base,
+                              uint8_t* tags, int32_t* codes, double* consts, cudaStream_t s) {
+  int64_t n = count * (int64_t)p.k;
+  if (n <= 0) return;
+  k_create_population<<<blocks_for(n), kThreads, 0, s>>>(p, count, stream_base, tags, codes, consts);
+  check_launch();
+}
+
+void launch_plan(const PlanParams& p, int64_t gen, const int64_t* gen_ptr, int64_t* u, int64_t* v,
+                 double* ms, int64_t stride_per_gen, cudaStream_t s) {
+  k_plan<<<blocks_for(p.m), kThreads, 0, s>>>(p, gen, gen_ptr, u, v, ms, stride_per_gen);
+  check_launch();
+}
+
+void launch_reduce_partials(const double* part, int64_t rows, int64_t ntiles, double* out,
+                            bool accumulate, cudaStream_t s) {
+  if (rows <= 0) return;
+  k_reduce_partials<<<(unsigned)rows, 128, 0, s>>>(part, ntiles, out, accumulate ? 1 : 0);
+  check_launch();
+}
+
+void launch_sum_shards(const double* const* in, int nshards, int64_t n, double* out, cudaStream_t s) {
+  GSGP_REQUIRE(nshards >= 1 && nshards <= 16, "1..16 local shards supported");
+  ShardPtrs sp{};
+  for (int i = 0; i < nshards; ++i) sp.p[i] = in[i];
+  k_sum_shards<<<blocks_for(n), kThreads, 0, s>>>(sp, nshards, n, out);
+  check_launch();
+}
+
+void launch_row_rmse(const double* S, const double* y, int64_t m, int64_t n, double* out,
+                     cudaStream_t s) {
+  if (m <= 0) return;
+  k_row_rmse<<<(unsigned)m, 256, 0, s>>>(S, y, n, out);
+  check_launch();
+}
+
+void launch_survive(const SurviveArgs& a, cudaStream_t s) {
+  k_survive<<<1, 1024, 0, s>>>(a);
+  check_launch();
+}
+
+void launch_init_state(const SurviveArgs& a, cudaStream_t s) {
+  k_init_state<<<1, 1024, 0, s>>>(a);
+  check_launch();
+}
+
+void launch_survive_decision(const double* fp, const double* fo, int64_t m, int64_t* out,
+                             cudaStream_t s) {
+  k_survive_decision<<<1, 1024, 0, s>>>(fp, fo, m, out);
+  check_launch();
+}
+
+}  // namespace gsgp

@@ -1,0 +1,59 @@
+"""Multi-GPU plumbing: one process per GPU, fitness cases sharded by rank.
+
+`torch.distributed` only bootstraps: rank 0 creates an NCCL unique id inside
+libgsgp_b200.so, it is broadcast over the existing process group, and every
+rank joins the library's own NCCL communicator (`gsgp_comm_init`).  After
+that `run_evolution` shards the train and test cases contiguously across
+ranks and the only per-generation collective is an NCCL allreduce of the
+[m][2] partial-SSE vector; genomes, plans and every survival
+decision are recomputed identically on each rank from the counter RNG.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from ._lib import check
+
+
+def shard_range(n: int, count: int, index: int) -> tuple[int, int]:
+    """Contiguous slice [lo, hi) of shard `index` out of `count` (same
+    formula as gsgp_shard_range in engine.cu)."""
+    return (n * index) // count, (n * (index + 1)) // count
+
+
+def init_from_torch(group=None) -> tuple[int, int]:
+    """Create the library's NCCL communicator over the ranks of an
+    initialised torch.distributed group; returns (world, rank)."""
+    import torch.distributed as td
+    world, rank = td.get_world_size(group), td.get_rank(group)
+    lib = _lib.load()
+    uid = (C.c_ubyte * 128)()
+    if rank == 0:
+        check(lib.gsgp_comm_unique_id(uid))
+    payload = [bytes(uid)]
+    td.broadcast_object_list(payload, src=0, group=group)
+    buf = (C.c_ubyte * 128).from_buffer_copy(payload[0])
+    check(lib.gsgp_comm_init(world, rank, buf))
+    return world, rank
+
+
+def destroy() -> None:
+    check(_lib.load().gsgp_comm_destroy())
+
+
+def gather_elite_semantics(result, n_train: int, group=None) -> np.ndarray:
+    """Assemble the full elite train semantics from every rank's slice."""
+    import torch
+    import torch.distributed as td
+    lo, hi = result.device["shard_train_range"]
+    local = torch.from_numpy(np.ascontiguousarray(result.elite_train_semantics[lo:hi]))
+    parts = [None] * td.get_world_size(group)
+    td.all_gather_object(parts, (lo, hi, local.numpy()), group=group)
+    full = np.zeros(n_train)
+    for a, b, vals in parts:
+        full[a:b] = vals
+    return full
