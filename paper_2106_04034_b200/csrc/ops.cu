@@ -189,7 +189,7 @@ constexpr ArgVal kMaxInit{-INFINITY, INT64_MAX};
 // gsgp/evolution.py:65-83 plus the loop bookkeeping at :146-158.
 // Slot flags (wide): a slot whose semantics overflowed fp32 at
 // initialisation keeps its (constant) fp64 fitness — see DESIGN.md §4.
-__global__ void k_survive(SurviveArgs a) {
+__global__ void __launch_bounds__(1024) k_survive(SurviveArgs a) {
   __shared__ ArgVal sh[32];
   __shared__ int64_t dec[4];
   const int64_t m = a.m;
@@ -250,7 +250,7 @@ __global__ void k_survive(SurviveArgs a) {
 }
 
 // evolution.py:132-143: initial fitness, elite and trace[0]
-__global__ void k_init_state(SurviveArgs a) {
+__global__ void __launch_bounds__(1024) k_init_state(SurviveArgs a) {
   __shared__ ArgVal sh[32];
   ArgVal b = kMinInit;
   for (int64_t i = threadIdx.x; i < a.m; i += blockDim.x) {
@@ -275,7 +275,8 @@ __global__ void k_init_state(SurviveArgs a) {
   }
 }
 
-__global__ void k_survive_decision(const double* fp, const double* fo, int64_t m, int64_t* out) {
+__global__ void __launch_bounds__(1024) k_survive_decision(const double* fp, const double* fo, int64_t m,
+                                                          int64_t* out) {
   __shared__ ArgVal sh[32];
   ArgVal bp = kMinInit, bo = kMinInit, wo = kMaxInit;
   for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
@@ -292,7 +293,7 @@ __global__ void k_survive_decision(const double* fp, const double* fo, int64_t m
   }
 }
 
-__global__ void k_argminmax(const double* f, int64_t m, int64_t* out) {
+__global__ void __launch_bounds__(1024) k_argminmax(const double* f, int64_t m, int64_t* out) {
   __shared__ ArgVal sh[32];
   ArgVal lo = kMinInit, hi = kMaxInit;
   for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {

@@ -17,7 +17,10 @@ def pytest_configure(config):
 
 
 def golden(name: str):
-    return np.load(GOLDEN / f"{name}.npz", allow_pickle=True)
+    path = GOLDEN / f"{name}.npz"
+    if not path.exists():
+        path = GOLDEN / f"run_{name}.npz"
+    return np.load(path, allow_pickle=True)
 
 
 def toy_dataset(n_cases=24, n_features=3, seed=0):
