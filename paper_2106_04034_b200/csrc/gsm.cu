@@ -5,21 +5,22 @@
 // with the reference's rounding order t = a -/+ b; t = t * ms; out = parent + t
 // (gsgp/mutation.py:77-83), applied to train AND test semantics with the same
 // plan in one pass (one row of storage = [train cases | pad | test cases | pad]),
-// followed by the fp64 squared error against the target (gsgp/fitness.py:23)
-// reduced per row: thread-sequential -> warp butterfly -> warps in order ->
-// tiles in order (k_reduce_partials).  The order is a function of case
-// positions only, so equal rows get bit-equal SSEs and argmin ties resolve to
-// the lowest index exactly like np.argmin.
+// followed by the fp64 squared error against the target (gsgp/fitness.py:23).
+// The SSE of each (row, case tile) is reduced in a fixed order —
+// thread-sequential -> warp butterfly -> warps in index order — and the tiles
+// are summed in index order by k_reduce_partials: a function of case positions
+// only, so equal rows get bit-equal SSEs and argmin ties resolve to the
+// lowest index exactly like np.argmin.
 //
-// Layout / traffic: row-major [rows][pitch] with pitch % 32 == 0, 128-bit
-// loads and stores.  The grid is case-tile-major (blockIdx -> (tile, row
-// group)), so all population rows of one case tile are processed close in
-// time and each pool row's tile segment is fetched from HBM once and then
-// served from L2 to the other rows that reference it: HBM traffic per
-// generation ~= 4*N*(2m + D + 1) bytes (D = distinct pool rows in the plan).
-// Parents are updated IN PLACE; the best parent row (ctl[CTL_BP]) is copied
-// aside while it streams by, and survival redirects the replaced slot to that
-// copy in the next generation, so no row copy kernel is needed.
+// Layout / traffic: row-major [rows][pitch] (pitch % 32 == 0).  Parents are
+// updated IN PLACE; the best parent row (ctl[CTL_BP]) is copied aside while
+// it streams by, and survival redirects the replaced slot to that copy in the
+// next generation (ctl[CTL_REDIRECT]), so no row-copy kernel is needed.
+// HBM traffic per generation ~= 4*N*(2m + D + 1) bytes, D = distinct pool
+// rows of the plan (each pool tile is read from HBM once, see below).
+#include <algorithm>
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace gsgp {
@@ -39,31 +40,103 @@ __device__ __forceinline__ double mut(double p, double a, double b, double ms, i
   return __dadd_rn(p, __dmul_rn(t, ms));
 }
 
-template <typename V> __device__ __forceinline__ V ld_stream(const V* p) { return *p; }
-template <> __device__ __forceinline__ float4 ld_stream(const float4* p) { return __ldcs(p); }
-template <> __device__ __forceinline__ double2 ld_stream(const double2* p) { return __ldcs(p); }
+// one work unit = (case tile, population row): 16 KB of each streamed row
+constexpr int kTileBytes = 16384;
 
-template <typename V> __device__ __forceinline__ V ld_pool(const V* p) { return __ldg(p); }
+// ===================================================================
+// TMA-pipelined persistent kernel (the engine's generation kernel).
+//
+// Units are numbered tile-major (unit = t*m + i) and dealt round-robin to
+// one persistent CTA per SM, so all CTAs sweep the case tiles in lockstep and
+// each pool tile is fetched from HBM once, then re-served from L2 to every
+// row that references it (pool copies: L2 evict_last; parent: evict_first;
+// offspring stores: streaming).
+//   warp 8  producer (one lane): per unit, 3 cp.async.bulk copies (parent
+//           row tile, pool[u] tile, pool[v] tile) into a kStages-deep
+//           shared-memory ring; completion = mbarrier transaction count.
+//   warps 0-7 consumers: copy the unit out of shared memory into registers,
+//           release the stage at once (so the producer refills it while
+//           they compute), mutate, store the offspring with 128-bit
+//           streaming stores, save the best parent row, and accumulate the
+//           fp64 SSE against the target, which each thread keeps in
+//           registers for as long as the CTA stays on the same case tile.
+//   warp 9  finalizer (one lane): folds the 8 per-warp SSE partials of each
+//           unit (fixed warp order) into part[i][t], decoupled from the
+//           consumers through a small mbarrier ring.
+// ===================================================================
+constexpr int kStages = 4;
+constexpr int kRedStages = 4;
+constexpr int kConsumerWarps = 8;
+constexpr int kNCT = kConsumerWarps * 32;
+constexpr int kTmaThreads = (kConsumerWarps + 2) * 32;
 
-constexpr int kThreads = 256;
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  const uint32_t a = smem_u32(bar);
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// global -> shared bulk copy on the TMA engine, completion on an mbarrier
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
 
 // kOp: operator mode (gsgp.gsm on arbitrary inputs): non-finite -> 0 with a
 // count (mutation.py:86).  In the engine the parent is finite (or an fp32
 // overflow slot whose fp64 value the reference keeps constant)
 // so no replacement is done there.
-template <typename T, bool kOp, int V, int R>
-__global__ void __launch_bounds__(kThreads, 2)
-k_gsm(GsmArgs a, int64_t ntiles, int64_t ngroups) {
+template <typename T, bool kOp>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t nunits) {
   using Vec = typename Vec16<T>::type;
   constexpr int EV = Vec16<T>::n;
-  constexpr int TILE = kThreads * V * EV;
-  __shared__ double red[kThreads / 32][R][2];
+  constexpr int TILE = kTileBytes / (int)sizeof(T);   // elements per unit
+  constexpr int VPT = TILE / (kNCT * EV);             // 16-byte vectors per consumer thread
+  static_assert(VPT * kNCT * EV == TILE, "tile must split evenly over consumers");
+  extern __shared__ __align__(128) unsigned char smem[];
+  T* data = reinterpret_cast<T*>(smem);                                   // [S][3][TILE]
+  double* red = reinterpret_cast<double*>(smem + kStages * 3 * kTileBytes);  // [RS][W][2]
+  uint64_t* full = reinterpret_cast<uint64_t*>(red + kRedStages * kConsumerWarps * 2);
+  uint64_t* empty = full + kStages;
+  uint64_t* rfull = empty + kStages;
+  uint64_t* rempty = rfull + kRedStages;
 
-  const int tid = threadIdx.x;
-  const int64_t tile = blockIdx.x / ngroups;          // case-tile-major order
-  const int64_t grp = blockIdx.x - tile * ngroups;
-  const int64_t i0 = grp * R;
-
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t m = a.m, G = gridDim.x;
   const int64_t* u = a.u;
   const int64_t* vv = a.v;
   const double* ms = a.ms;
@@ -72,89 +145,250 @@ k_gsm(GsmArgs a, int64_t ntiles, int64_t ngroups) {
   T* elite_cur = reinterpret_cast<T*>(a.elite_cur);
   if (a.ctl) {
     const int64_t gen = a.ctl[CTL_GEN];
-    const int64_t par = a.ctl[CTL_PARITY];
     bp = a.ctl[CTL_BP];
     redirect = a.ctl[CTL_REDIRECT];
-    u += (gen - 1) * a.m;
-    vv += (gen - 1) * a.m;
-    ms += (gen - 1) * a.m;
-    if (par) {   // ping-pong elite buffers
+    u += (gen - 1) * m;
+    vv += (gen - 1) * m;
+    ms += (gen - 1) * m;
+    if (a.ctl[CTL_PARITY]) {   // ping-pong elite buffers
       const T* t0 = elite_prev;
       elite_prev = elite_cur;
       elite_cur = const_cast<T*>(t0);
     }
   }
-
-  int64_t e[V];
-  bool ok[V], tr[V];
-  double y[V][EV];
-#pragma unroll
-  for (int v = 0; v < V; ++v) {
-    e[v] = tile * TILE + ((int64_t)v * kThreads + tid) * EV;
-    ok[v] = e[v] < a.pitch;
-    tr[v] = e[v] < a.test_off;
-#pragma unroll
-    for (int c = 0; c < EV; ++c) y[v][c] = ok[v] ? a.y[e[v] + c] : 0.0;
-  }
-
   const T* pool = reinterpret_cast<const T*>(a.pool);
   T* S = reinterpret_cast<T*>(a.S);
-  unsigned long long nonfinite = 0;
-  double acc_tr[R], acc_te[R];
 
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    acc_tr[r] = 0.0;
-    acc_te[r] = 0.0;
-    const int64_t i = i0 + r;
-    if (i >= a.m) continue;
-    const int64_t ui = u[i], vi = vv[i];
-    const T msv = (T)ms[i];
-    const T* prow = (i == redirect) ? elite_prev : S + i * a.pitch;
-    const Vec* pu = reinterpret_cast<const Vec*>(pool + ui * a.pitch);
-    const Vec* pv = reinterpret_cast<const Vec*>(pool + vi * a.pitch);
-    const Vec* pp = reinterpret_cast<const Vec*>(prow);
-    Vec* po = reinterpret_cast<Vec*>(S + i * a.pitch);
-    Vec P[V], A[V], Bv[V];
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      if (!ok[v]) continue;
-      const int64_t w = e[v] / EV;
-      P[v] = ld_stream(pp + w);
-      A[v] = ld_pool(pu + w);
-      Bv[v] = ld_pool(pv + w);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, kConsumerWarps);
     }
+    for (int s = 0; s < kRedStages; ++s) {
+      mbar_init(rfull + s, kConsumerWarps);
+      mbar_init(rempty + s, 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  // unit sequence of this CTA: unit_k = blockIdx.x + k*G, tracked as (t, i)
+  const int64_t i_step = G % m, t_step = G / m;
+  const int64_t i_first = (int64_t)blockIdx.x % m, t_first = (int64_t)blockIdx.x / m;
+
+  if (warp == kConsumerWarps) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      const uint64_t keep = l2_policy_evict_last(), stream = l2_policy_evict_first();
+      int64_t t = t_first, i = i_first;
+      int s = 0;
+      uint32_t j = 0;
+      for (int64_t unit = blockIdx.x, k = 0; unit < nunits; unit += G, ++k) {
+        const int64_t off = t * TILE;
+        const int64_t n = min((int64_t)TILE, a.pitch - off);
+        if (k >= kStages) mbar_wait(empty + s, (j & 1) ^ 1);
+        const int64_t ui = u[i], vi = vv[i];
+        const T* src = (i == redirect) ? elite_prev : S + i * a.pitch;
+        const uint32_t bytes = (uint32_t)(n * sizeof(T));
+        T* d = data + (int64_t)s * 3 * TILE;
+        mbar_expect_tx(full + s, 3 * bytes);
+        bulk_g2s(d, src + off, bytes, full + s, stream);
+        bulk_g2s(d + TILE, pool + ui * a.pitch + off, bytes, full + s, keep);
+        bulk_g2s(d + 2 * TILE, pool + vi * a.pitch + off, bytes, full + s, keep);
+        if (++s == kStages) { s = 0; ++j; }
+        i += i_step; t += t_step;
+        if (i >= m) { i -= m; ++t; }
+      }
+    }
+    return;
+  }
+  if (warp == kConsumerWarps + 1) {
+    // ----------------------------------------------------------- finalizer
+    if (lane == 0) {
+      int64_t t = t_first, i = i_first;
+      int rs = 0;
+      uint32_t rj = 0;
+      for (int64_t unit = blockIdx.x; unit < nunits; unit += G) {
+        mbar_wait(rfull + rs, rj & 1);
+        const double* r = red + rs * kConsumerWarps * 2;
+        double x = 0.0, z = 0.0;
 #pragma unroll
-    for (int v = 0; v < V; ++v) {
-      if (!ok[v]) continue;
-      const int64_t w = e[v] / EV;
-      T* pe = reinterpret_cast<T*>(&P[v]);
-      T* ae = reinterpret_cast<T*>(&A[v]);
-      T* be = reinterpret_cast<T*>(&Bv[v]);
+        for (int w = 0; w < kConsumerWarps; ++w) {
+          x = __dadd_rn(x, r[2 * w]);
+          z = __dadd_rn(z, r[2 * w + 1]);
+        }
+        mbar_arrive(rempty + rs);
+        a.part[(i * ntiles + t) * 2] = x;
+        a.part[(i * ntiles + t) * 2 + 1] = z;
+        if (++rs == kRedStages) { rs = 0; ++rj; }
+        i += i_step; t += t_step;
+        if (i >= m) { i -= m; ++t; }
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  const int ct = threadIdx.x;   // 0 .. kNCT-1
+  int64_t t = t_first, i = i_first, cur_t = -1;
+  int s = 0, rs = 0;
+  uint32_t j = 0, rj = 0;
+  double y[VPT][EV];
+  unsigned long long nonfinite = 0;
+  for (int64_t unit = blockIdx.x, k = 0; unit < nunits; unit += G, ++k) {
+    const int64_t off = t * TILE;
+    const int64_t n = min((int64_t)TILE, a.pitch - off);
+    if (t != cur_t) {   // target tile: registers, reloaded when the CTA changes tile
+#pragma unroll
+      for (int q = 0; q < VPT; ++q) {
+        const int64_t e = (int64_t)(q * kNCT + ct) * EV;
+#pragma unroll
+        for (int c = 0; c < EV; ++c) y[q][c] = e < n ? __ldg(a.y + off + e + c) : 0.0;
+      }
+      cur_t = t;
+    }
+    const T msv = (T)ms[i];
+    const bool save = (i == bp);
+    mbar_wait(full + s, j & 1);
+    const T* d = data + (int64_t)s * 3 * TILE;
+    Vec P[VPT], A[VPT], B[VPT];
+#pragma unroll
+    for (int q = 0; q < VPT; ++q) {
+      const int e = (q * kNCT + ct) * EV;
+      P[q] = *reinterpret_cast<const Vec*>(d + e);
+      A[q] = *reinterpret_cast<const Vec*>(d + TILE + e);
+      B[q] = *reinterpret_cast<const Vec*>(d + 2 * TILE + e);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + s);   // stage free: the producer refills while we compute
+    if (++s == kStages) { s = 0; ++j; }
+
+    T* orow = S + i * a.pitch + off;
+    double acc_tr = 0.0, acc_te = 0.0;
+#pragma unroll
+    for (int q = 0; q < VPT; ++q) {
+      const int e = (q * kNCT + ct) * EV;
+      if (e >= n) continue;
+      const T* pe = reinterpret_cast<const T*>(&P[q]);
+      const T* ae = reinterpret_cast<const T*>(&A[q]);
+      const T* be = reinterpret_cast<const T*>(&B[q]);
       Vec O;
       T* oe = reinterpret_cast<T*>(&O);
-      double s = 0.0;
+      double sacc = 0.0;
 #pragma unroll
       for (int c = 0; c < EV; ++c) {
         T o = mut(pe[c], ae[c], be[c], msv, a.sign);
         if (kOp && !isfinite((double)o)) { o = (T)0; ++nonfinite; }
         oe[c] = o;
-        double d = __dsub_rn((double)o, y[v][c]);
-        s = __dadd_rn(s, __dmul_rn(d, d));
+        const double dd = __dsub_rn((double)o, y[q][c]);
+        sacc = __dadd_rn(sacc, __dmul_rn(dd, dd));
       }
-      po[w] = O;
-      if (i == bp) reinterpret_cast<Vec*>(elite_cur)[w] = P[v];
-      if (tr[v]) acc_tr[r] = __dadd_rn(acc_tr[r], s);
-      else acc_te[r] = __dadd_rn(acc_te[r], s);
+      __stcs(reinterpret_cast<Vec*>(orow + e), O);
+      if (save) __stcs(reinterpret_cast<Vec*>(elite_cur + off + e), P[q]);
+      if (off + e < a.test_off) acc_tr = __dadd_rn(acc_tr, sacc);
+      else acc_te = __dadd_rn(acc_te, sacc);
+    }
+    // fixed-order warp reduction; a unit wholly in train (or test) needs one
+    if (off + n <= a.test_off) acc_tr = warp_sum(acc_tr);
+    else if (off >= a.test_off) acc_te = warp_sum(acc_te);
+    else { acc_tr = warp_sum(acc_tr); acc_te = warp_sum(acc_te); }
+    if (lane == 0) {
+      if (k >= kRedStages) mbar_wait(rempty + rs, (rj & 1) ^ 1);
+      red[(rs * kConsumerWarps + warp) * 2] = acc_tr;
+      red[(rs * kConsumerWarps + warp) * 2 + 1] = acc_te;
+      mbar_arrive(rfull + rs);
+    }
+    if (++rs == kRedStages) { rs = 0; ++rj; }
+    i += i_step; t += t_step;
+    if (i >= m) { i -= m; ++t; }
+  }
+  if (kOp) {
+    for (int o = 16; o > 0; o >>= 1) nonfinite += __shfl_xor_sync(0xffffffffu, nonfinite, o);
+    if (lane == 0 && nonfinite) atomicAdd(a.nonfinite, nonfinite);
+  }
+}
+
+constexpr size_t kTmaSmem = (size_t)kStages * 3 * kTileBytes + (size_t)kRedStages * kConsumerWarps * 2 * 8 +
+                            (2 * kStages + 2 * kRedStages) * 8;
+
+// ===================================================================
+// Plain-load variant kept only for A/B measurement (GSGP_GSM_LEGACY=1):
+// blockIdx -> (tile, group of kRowsPerBlock rows), 128-bit loads.
+// ===================================================================
+constexpr int kThreads = 256;
+constexpr int kRowsPerBlock = 8;
+
+template <typename T, bool kOp>
+__global__ void __launch_bounds__(kThreads, 2) k_gsm_plain(GsmArgs a, int64_t ntiles, int64_t ngroups) {
+  using Vec = typename Vec16<T>::type;
+  constexpr int EV = Vec16<T>::n;
+  constexpr int TILE = kTileBytes / (int)sizeof(T);
+  constexpr int V = TILE / (kThreads * EV);
+  constexpr int R = kRowsPerBlock;
+  __shared__ double red[kThreads / 32][R][2];
+  const int tid = threadIdx.x;
+  const int64_t tile = blockIdx.x / ngroups;
+  const int64_t i0 = (blockIdx.x - tile * ngroups) * R;
+  const int64_t* u = a.u;
+  const int64_t* vv = a.v;
+  const double* ms = a.ms;
+  int64_t bp = -1, redirect = -1;
+  const T* elite_prev = reinterpret_cast<const T*>(a.elite_prev);
+  T* elite_cur = reinterpret_cast<T*>(a.elite_cur);
+  if (a.ctl) {
+    const int64_t gen = a.ctl[CTL_GEN];
+    bp = a.ctl[CTL_BP];
+    redirect = a.ctl[CTL_REDIRECT];
+    u += (gen - 1) * a.m;
+    vv += (gen - 1) * a.m;
+    ms += (gen - 1) * a.m;
+    if (a.ctl[CTL_PARITY]) {
+      const T* t0 = elite_prev;
+      elite_prev = elite_cur;
+      elite_cur = const_cast<T*>(t0);
     }
   }
-  // per-row fixed-order block reduction
+  const T* pool = reinterpret_cast<const T*>(a.pool);
+  T* S = reinterpret_cast<T*>(a.S);
+  unsigned long long nonfinite = 0;
   const int warp = tid >> 5, lane = tid & 31;
-#pragma unroll
   for (int r = 0; r < R; ++r) {
-    double x = warp_sum(acc_tr[r]);
-    double z = warp_sum(acc_te[r]);
-    if (lane == 0) { red[warp][r][0] = x; red[warp][r][1] = z; }
+    const int64_t i = i0 + r;
+    double acc_tr = 0.0, acc_te = 0.0;
+    if (i < a.m) {
+      const T msv = (T)ms[i];
+      const T* prow = (i == redirect) ? elite_prev : S + i * a.pitch;
+      const T* pu = pool + u[i] * a.pitch;
+      const T* pv = pool + vv[i] * a.pitch;
+#pragma unroll
+      for (int q = 0; q < V; ++q) {
+        const int64_t e = tile * TILE + (int64_t)(q * kThreads + tid) * EV;
+        if (e >= a.pitch) continue;
+        const Vec P = __ldcs(reinterpret_cast<const Vec*>(prow + e));
+        const Vec A = __ldg(reinterpret_cast<const Vec*>(pu + e));
+        const Vec B = __ldg(reinterpret_cast<const Vec*>(pv + e));
+        const T* pe = reinterpret_cast<const T*>(&P);
+        const T* ae = reinterpret_cast<const T*>(&A);
+        const T* be = reinterpret_cast<const T*>(&B);
+        Vec O;
+        T* oe = reinterpret_cast<T*>(&O);
+        double sacc = 0.0;
+        for (int c = 0; c < EV; ++c) {
+          T o = mut(pe[c], ae[c], be[c], msv, a.sign);
+          if (kOp && !isfinite((double)o)) { o = (T)0; ++nonfinite; }
+          oe[c] = o;
+          const double dd = __dsub_rn((double)o, __ldg(a.y + e + c));
+          sacc = __dadd_rn(sacc, __dmul_rn(dd, dd));
+        }
+        *reinterpret_cast<Vec*>(S + i * a.pitch + e) = O;
+        if (i == bp) *reinterpret_cast<Vec*>(elite_cur + e) = P;
+        if (e < a.test_off) acc_tr = __dadd_rn(acc_tr, sacc);
+        else acc_te = __dadd_rn(acc_te, sacc);
+      }
+    }
+    acc_tr = warp_sum(acc_tr);
+    acc_te = warp_sum(acc_te);
+    if (lane == 0) { red[warp][r][0] = acc_tr; red[warp][r][1] = acc_te; }
   }
   __syncthreads();
   if (tid < 2 * R) {
@@ -162,7 +396,6 @@ k_gsm(GsmArgs a, int64_t ntiles, int64_t ngroups) {
     const int64_t i = i0 + r;
     if (i < a.m) {
       double t = 0.0;
-#pragma unroll
       for (int w = 0; w < kThreads / 32; ++w) t = __dadd_rn(t, red[w][r][w2]);
       a.part[(i * ntiles + tile) * 2 + w2] = t;
     }
@@ -173,14 +406,12 @@ k_gsm(GsmArgs a, int64_t ntiles, int64_t ngroups) {
   }
 }
 
-constexpr int kRowsPerBlock = 8;
-constexpr int kVecF32 = 2;   // 2 x float4 per thread per row: tile = 2048 cases
-constexpr int kVecF64 = 4;   // 4 x double2: tile = 2048 cases
+int g_num_sms = 0;
 
 }  // namespace
 
 int64_t gsm_tiles(int64_t pitch, bool f64) {
-  const int64_t tile = f64 ? kThreads * kVecF64 * 2 : kThreads * kVecF32 * 4;
+  const int64_t tile = kTileBytes / (f64 ? 8 : 4);
   return (pitch + tile - 1) / tile;
 }
 
@@ -188,20 +419,30 @@ void launch_gsm(const GsmArgs& a, bool f64, bool operator_mode, cudaStream_t s) 
   if (a.m <= 0 || a.pitch <= 0) return;
   GSGP_REQUIRE(a.pitch % 32 == 0, "storage pitch must be a multiple of 32");
   const int64_t ntiles = gsm_tiles(a.pitch, f64);
-  const int64_t ngroups = (a.m + kRowsPerBlock - 1) / kRowsPerBlock;
-  const int64_t blocks = ntiles * ngroups;
-  GSGP_REQUIRE(blocks < (1ll << 31), "generation grid too large");
-  if (f64) {
-    if (operator_mode)
-      k_gsm<double, true, kVecF64, kRowsPerBlock><<<(unsigned)blocks, kThreads, 0, s>>>(a, ntiles, ngroups);
-    else
-      k_gsm<double, false, kVecF64, kRowsPerBlock><<<(unsigned)blocks, kThreads, 0, s>>>(a, ntiles, ngroups);
-  } else {
-    if (operator_mode)
-      k_gsm<float, true, kVecF32, kRowsPerBlock><<<(unsigned)blocks, kThreads, 0, s>>>(a, ntiles, ngroups);
-    else
-      k_gsm<float, false, kVecF32, kRowsPerBlock><<<(unsigned)blocks, kThreads, 0, s>>>(a, ntiles, ngroups);
+  static const bool legacy = getenv("GSGP_GSM_LEGACY") != nullptr;   // A/B measurement only
+  if (legacy) {
+    const int64_t ngroups = (a.m + kRowsPerBlock - 1) / kRowsPerBlock;
+    const int64_t blocks = ntiles * ngroups;
+    GSGP_REQUIRE(blocks < (1ll << 31), "generation grid too large");
+    auto go = [&](auto kern) { kern<<<(unsigned)blocks, kThreads, 0, s>>>(a, ntiles, ngroups); };
+    if (f64) operator_mode ? go(k_gsm_plain<double, true>) : go(k_gsm_plain<double, false>);
+    else operator_mode ? go(k_gsm_plain<float, true>) : go(k_gsm_plain<float, false>);
+    GSGP_CUDA(cudaGetLastError());
+    return;
   }
+  if (g_num_sms == 0) {
+    int dev = 0;
+    GSGP_CUDA(cudaGetDevice(&dev));
+    GSGP_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const int64_t nunits = ntiles * a.m;
+  const unsigned grid = (unsigned)std::min<int64_t>(g_num_sms, nunits);
+  auto go = [&](auto kern) {
+    GSGP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
+    kern<<<grid, kTmaThreads, kTmaSmem, s>>>(a, ntiles, nunits);
+  };
+  if (f64) operator_mode ? go(k_gsm_tma<double, true>) : go(k_gsm_tma<double, false>);
+  else operator_mode ? go(k_gsm_tma<float, true>) : go(k_gsm_tma<float, false>);
   GSGP_CUDA(cudaGetLastError());
 }
 
