@@ -167,7 +167,7 @@ inline unsigned nblk(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t
 struct Shard {
   int64_t tr_lo = 0, tr_hi = 0, te_lo = 0, te_hi = 0;
   int64_t ntr = 0, nte = 0, pitch = 0, test_off = 0, ntiles = 0;
-  DevBuf S, pool, elite[2], y_store, part, sse;
+  DevBuf S, pool, elite[2], y_store, part, sse, ticket;
 };
 
 void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, int64_t ntr,
@@ -282,6 +282,7 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
     p->y_store.alloc(p->pitch * 8);
     p->part.alloc(m * p->ntiles * 2 * 8);
     p->sse.alloc(m * 2 * 8);
+    p->ticket.alloc(8);
     GSGP_CUDA(cudaMemsetAsync(p->S.p, 0, m * p->pitch * esz, st));
     GSGP_CUDA(cudaMemsetAsync(p->pool.p, 0, r * p->pitch * esz, st));
     GSGP_CUDA(cudaMemsetAsync(p->elite[0].p, 0, p->pitch * esz, st));
@@ -415,6 +416,7 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
       a.ctl = ctl.as<int64_t>();
       a.sign = cfg->gsm_sign;
       a.part = p->part.as<double>();
+      a.ticket = p->ticket.as<unsigned long long>();
       launch_gsm(a, f64, false, s);
       ++n;
     }

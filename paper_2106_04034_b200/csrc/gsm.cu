@@ -134,9 +134,11 @@ k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t nunits) {
   uint64_t* empty = full + kStages;
   uint64_t* rfull = empty + kStages;
   uint64_t* rempty = rfull + kRedStages;
+  int64_t* slot_unit = reinterpret_cast<int64_t*>(rempty + kRedStages);   // [S] unit in stage
+  int64_t* red_unit = slot_unit + kStages;                                // [RS] unit in red slot
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t m = a.m, G = gridDim.x;
+  const int64_t m = a.m;
   const int64_t* u = a.u;
   const int64_t* vv = a.v;
   const double* ms = a.ms;
@@ -172,32 +174,50 @@ k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t nunits) {
   }
   __syncthreads();
 
-  // unit sequence of this CTA: unit_k = blockIdx.x + k*G, tracked as (t, i)
-  const int64_t i_step = G % m, t_step = G / m;
-  const int64_t i_first = (int64_t)blockIdx.x % m, t_first = (int64_t)blockIdx.x / m;
-
+  // Units are handed out dynamically, in tile-major order, from a global
+  // ticket counter: every CTA always works on the globally next units, so
+  // the CTAs cannot drift apart over a long kernel and the pool tiles in use
+  // stay L2-resident (a static round-robin split drifted by many tiles at
+  // 10M cases).  The producer publishes each unit id in slot_unit[stage];
+  // -1 terminates the consumers, who forward it to the finalizer.
   if (warp == kConsumerWarps) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       const uint64_t keep = l2_policy_evict_last(), stream = l2_policy_evict_first();
-      int64_t t = t_first, i = i_first;
       int s = 0;
       uint32_t j = 0;
-      for (int64_t unit = blockIdx.x, k = 0; unit < nunits; unit += G, ++k) {
+      // tickets are claimed kBatch units at a time, one claim ahead, so the
+      // atomic's round trip overlaps the current units' copies
+      constexpr int kBatch = 2;
+      int64_t next = (int64_t)atomicAdd(a.ticket, (unsigned long long)kBatch);
+      int64_t base = 0;
+      int in_batch = kBatch;
+      for (int64_t k = 0;; ++k) {
+        if (in_batch == kBatch) {
+          base = next;
+          in_batch = 0;
+          if (base < nunits) next = (int64_t)atomicAdd(a.ticket, (unsigned long long)kBatch);
+        }
+        const int64_t unit = base + in_batch++;
+        if (k >= kStages) mbar_wait(empty + s, (j & 1) ^ 1);
+        if (unit >= nunits) {
+          slot_unit[s] = -1;
+          mbar_arrive(full + s);
+          break;
+        }
+        const int64_t t = unit / m, i = unit - t * m;
         const int64_t off = t * TILE;
         const int64_t n = min((int64_t)TILE, a.pitch - off);
-        if (k >= kStages) mbar_wait(empty + s, (j & 1) ^ 1);
         const int64_t ui = u[i], vi = vv[i];
         const T* src = (i == redirect) ? elite_prev : S + i * a.pitch;
         const uint32_t bytes = (uint32_t)(n * sizeof(T));
         T* d = data + (int64_t)s * 3 * TILE;
+        slot_unit[s] = unit;
         mbar_expect_tx(full + s, 3 * bytes);
         bulk_g2s(d, src + off, bytes, full + s, stream);
         bulk_g2s(d + TILE, pool + ui * a.pitch + off, bytes, full + s, keep);
         bulk_g2s(d + 2 * TILE, pool + vi * a.pitch + off, bytes, full + s, keep);
         if (++s == kStages) { s = 0; ++j; }
-        i += i_step; t += t_step;
-        if (i >= m) { i -= m; ++t; }
       }
     }
     return;
@@ -205,11 +225,12 @@ k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t nunits) {
   if (warp == kConsumerWarps + 1) {
     // ----------------------------------------------------------- finalizer
     if (lane == 0) {
-      int64_t t = t_first, i = i_first;
       int rs = 0;
       uint32_t rj = 0;
-      for (int64_t unit = blockIdx.x; unit < nunits; unit += G) {
+      for (;;) {
         mbar_wait(rfull + rs, rj & 1);
+        const int64_t unit = red_unit[rs];
+        if (unit < 0) break;
         const double* r = red + rs * kConsumerWarps * 2;
         double x = 0.0, z = 0.0;
 #pragma unroll
@@ -218,11 +239,10 @@ k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t nunits) {
           z = __dadd_rn(z, r[2 * w + 1]);
         }
         mbar_arrive(rempty + rs);
+        const int64_t t = unit / m, i = unit - t * m;
         a.part[(i * ntiles + t) * 2] = x;
         a.part[(i * ntiles + t) * 2 + 1] = z;
         if (++rs == kRedStages) { rs = 0; ++rj; }
-        i += i_step; t += t_step;
-        if (i >= m) { i -= m; ++t; }
       }
     }
     return;
@@ -230,12 +250,23 @@ k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t nunits) {
 
   // -------------------------------------------------------------- consumers
   const int ct = threadIdx.x;   // 0 .. kNCT-1
-  int64_t t = t_first, i = i_first, cur_t = -1;
+  int64_t cur_t = -1;
   int s = 0, rs = 0;
   uint32_t j = 0, rj = 0;
   double y[VPT][EV];
   unsigned long long nonfinite = 0;
-  for (int64_t unit = blockIdx.x, k = 0; unit < nunits; unit += G, ++k) {
+  for (int64_t k = 0;; ++k) {
+    mbar_wait(full + s, j & 1);
+    const int64_t unit = slot_unit[s];
+    if (unit < 0) {   // no more units: tell the finalizer and stop
+      if (lane == 0) {
+        if (k >= kRedStages) mbar_wait(rempty + rs, (rj & 1) ^ 1);
+        if (warp == 0) red_unit[rs] = -1;
+        mbar_arrive(rfull + rs);
+      }
+      break;
+    }
+    const int64_t t = unit / m, i = unit - t * m;
     const int64_t off = t * TILE;
     const int64_t n = min((int64_t)TILE, a.pitch - off);
     if (t != cur_t) {   // target tile: registers, reloaded when the CTA changes tile
@@ -249,7 +280,6 @@ k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t nunits) {
     }
     const T msv = (T)ms[i];
     const bool save = (i == bp);
-    mbar_wait(full + s, j & 1);
     const T* d = data + (int64_t)s * 3 * TILE;
     Vec P[VPT], A[VPT], B[VPT];
 #pragma unroll
@@ -296,11 +326,10 @@ k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t nunits) {
       if (k >= kRedStages) mbar_wait(rempty + rs, (rj & 1) ^ 1);
       red[(rs * kConsumerWarps + warp) * 2] = acc_tr;
       red[(rs * kConsumerWarps + warp) * 2 + 1] = acc_te;
+      if (warp == 0) red_unit[rs] = unit;
       mbar_arrive(rfull + rs);
     }
     if (++rs == kRedStages) { rs = 0; ++rj; }
-    i += i_step; t += t_step;
-    if (i >= m) { i -= m; ++t; }
   }
   if (kOp) {
     for (int o = 16; o > 0; o >>= 1) nonfinite += __shfl_xor_sync(0xffffffffu, nonfinite, o);
@@ -309,7 +338,7 @@ k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t nunits) {
 }
 
 constexpr size_t kTmaSmem = (size_t)kStages * 3 * kTileBytes + (size_t)kRedStages * kConsumerWarps * 2 * 8 +
-                            (2 * kStages + 2 * kRedStages) * 8;
+                            (2 * kStages + 2 * kRedStages) * 8 + (kStages + kRedStages) * 8;
 
 // ===================================================================
 // Plain-load variant kept only for A/B measurement (GSGP_GSM_LEGACY=1):
@@ -437,6 +466,8 @@ void launch_gsm(const GsmArgs& a, bool f64, bool operator_mode, cudaStream_t s) 
   }
   const int64_t nunits = ntiles * a.m;
   const unsigned grid = (unsigned)std::min<int64_t>(g_num_sms, nunits);
+  GSGP_REQUIRE(a.ticket != nullptr, "GSM launch needs a ticket counter");
+  GSGP_CUDA(cudaMemsetAsync(a.ticket, 0, sizeof(unsigned long long), s));
   auto go = [&](auto kern) {
     GSGP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
     kern<<<grid, kTmaThreads, kTmaSmem, s>>>(a, ntiles, nunits);

@@ -91,6 +91,7 @@ struct GsmArgs {
   int32_t sign;             // 0 minus, 1 plus
   double* part;             // [m][ntiles][2]
   unsigned long long* nonfinite;   // operator mode only
+  unsigned long long* ticket;      // dynamic unit dispatch counter (zeroed per launch)
 };
 int64_t gsm_tiles(int64_t pitch, bool f64);
 void launch_gsm(const GsmArgs& a, bool f64, bool operator_mode, cudaStream_t s);
