@@ -290,7 +290,8 @@ int gsgp_gsm(const double* parent, int64_t m, int64_t n, const double* trees, in
     a.sign = sign;
     a.part = part.as<double>();
     a.nonfinite = nf.as<unsigned long long>();
-    Buf ticket(8);
+    Buf ticket(16);
+    GSGP_CUDA(cudaMemset(ticket.p, 0, 16));
     a.ticket = ticket.as<unsigned long long>();
     launch_gsm(a, true, true, 0);
     GSGP_CUDA(cudaMemcpy2D(out, n * 8, P.p, pitch * 8, n * 8, m, cudaMemcpyDeviceToHost));
@@ -345,7 +346,8 @@ int gsgp_gsm_step_f32(const float* parent_tr, const float* parent_te, const floa
     a.ms = dm.as<double>();
     a.sign = sign;
     a.part = part.as<double>();
-    Buf ticket(8);
+    Buf ticket(16);
+    GSGP_CUDA(cudaMemset(ticket.p, 0, 16));
     a.ticket = ticket.as<unsigned long long>();
     launch_gsm(a, false, false, 0);
     launch_reduce_partials(part.as<double>(), m, ntiles, sse.as<double>(), false, 0);

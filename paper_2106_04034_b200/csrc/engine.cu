@@ -282,7 +282,8 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
     p->y_store.alloc(p->pitch * 8);
     p->part.alloc(m * p->ntiles * 2 * 8);
     p->sse.alloc(m * 2 * 8);
-    p->ticket.alloc(8);
+    p->ticket.alloc(16);
+    GSGP_CUDA(cudaMemsetAsync(p->ticket.p, 0, 16, st));
     GSGP_CUDA(cudaMemsetAsync(p->S.p, 0, m * p->pitch * esz, st));
     GSGP_CUDA(cudaMemsetAsync(p->pool.p, 0, r * p->pitch * esz, st));
     GSGP_CUDA(cudaMemsetAsync(p->elite[0].p, 0, p->pitch * esz, st));
@@ -394,12 +395,18 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   const bool timed = cfg->time_kernels != 0;
   std::vector<std::unique_ptr<Event>> tev;
   int64_t launches_per_gen = 0;
+  DevBuf done;
+  done.alloc(16);
+  GSGP_CUDA(cudaMemsetAsync(done.p, 0, 16, st));
+  const bool fused_tail = (G == 1 && W == 1);
+  // one generation: GSM+SSE with the plan drawn inline (per shard), then the
+  // SSE tile reduction and survival — fused into one kernel when there is a
+  // single shard, else reduce per shard -> exchange -> survive
   auto enqueue_generation = [&](cudaStream_t s, Event* t0, Event* t1) {
     int64_t n = 0;
-    launch_plan(pp, 0, ctl.as<int64_t>(), pu.as<int64_t>(), pv.as<int64_t>(), pms.as<double>(), m, s);
-    ++n;
     if (t0) GSGP_CUDA(cudaEventRecord(t0->e, s));
-    for (auto& p : sh) {
+    for (size_t si = 0; si < sh.size(); ++si) {
+      auto& p = sh[si];
       if (p->pitch == 0) continue;
       GsmArgs a{};
       a.pool = p->pool.p;
@@ -417,19 +424,27 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
       a.sign = cfg->gsm_sign;
       a.part = p->part.as<double>();
       a.ticket = p->ticket.as<unsigned long long>();
+      a.plan_inline = 1;
+      a.write_plan = si == 0 ? 1 : 0;
+      a.plan = pp;
       launch_gsm(a, f64, false, s);
       ++n;
     }
     if (t1) GSGP_CUDA(cudaEventRecord(t1->e, s));
-    for (auto& p : sh) {
-      if (p->pitch == 0) continue;
-      launch_reduce_partials(p->part.as<double>(), m, p->ntiles, p->sse.as<double>(), false, s);
+    if (fused_tail && sh[0]->pitch > 0) {
+      launch_reduce_survive(sh[0]->part.as<double>(), sh[0]->ntiles, sse_vec, sa, done.as<unsigned int>(), s);
+      ++n;
+    } else {
+      for (auto& p : sh) {
+        if (p->pitch == 0) continue;
+        launch_reduce_partials(p->part.as<double>(), m, p->ntiles, p->sse.as<double>(), false, s);
+        ++n;
+      }
+      exchange(s);
+      n += (G > 1) ? 1 : 0;
+      launch_survive(sa, s);
       ++n;
     }
-    exchange(s);
-    n += (G > 1) ? 1 : 0;
-    launch_survive(sa, s);
-    ++n;
     launches_per_gen = n;
   };
   // timing window: generations (w0, g]; ev_win0 is recorded after generation w0

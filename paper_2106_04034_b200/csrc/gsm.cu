@@ -46,14 +46,16 @@ constexpr int kTileBytes = 16384;
 // ===================================================================
 // TMA-pipelined persistent kernel (the engine's generation kernel).
 //
-// Units are numbered tile-major (unit = t*m + i) and dealt round-robin to
-// one persistent CTA per SM, so all CTAs sweep the case tiles in lockstep and
-// each pool tile is fetched from HBM once, then re-served from L2 to every
-// row that references it (pool copies: L2 evict_last; parent: evict_first;
-// offspring stores: streaming).
-//   warp 8  producer (one lane): per unit, 3 cp.async.bulk copies (parent
-//           row tile, pool[u] tile, pool[v] tile) into a kStages-deep
-//           shared-memory ring; completion = mbarrier transaction count.
+// Units are numbered tile-major (unit = t*m + i) and handed out from a
+// global ticket counter to one persistent CTA per SM, so all CTAs sweep the
+// case tiles in lockstep and each pool tile is fetched from HBM once, then
+// re-served from L2 to every row that references it (pool copies: L2
+// evict_last; parent: evict_first; offspring stores: streaming).
+//   warp 8  producer (one lane): claims units, draws the row's mutation plan
+//           (u, v, ms) from the counter RNG, and issues 3 cp.async.bulk
+//           copies (parent row tile, pool[u] tile, pool[v] tile) into a
+//           kStages-deep shared-memory ring; completion = mbarrier
+//           transaction count.
 //   warps 0-7 consumers: copy the unit out of shared memory into registers,
 //           release the stage at once (so the producer refills it while
 //           they compute), mutate, store the offspring with 128-bit
@@ -136,17 +138,18 @@ k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t nunits) {
   uint64_t* rempty = rfull + kRedStages;
   int64_t* slot_unit = reinterpret_cast<int64_t*>(rempty + kRedStages);   // [S] unit in stage
   int64_t* red_unit = slot_unit + kStages;                                // [RS] unit in red slot
+  double* slot_ms = reinterpret_cast<double*>(red_unit + kRedStages);     // [S] mutation step
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t m = a.m;
   const int64_t* u = a.u;
   const int64_t* vv = a.v;
   const double* ms = a.ms;
-  int64_t bp = -1, redirect = -1;
+  int64_t bp = -1, redirect = -1, gen = 0;
   const T* elite_prev = reinterpret_cast<const T*>(a.elite_prev);
   T* elite_cur = reinterpret_cast<T*>(a.elite_cur);
   if (a.ctl) {
-    const int64_t gen = a.ctl[CTL_GEN];
+    gen = a.ctl[CTL_GEN];
     bp = a.ctl[CTL_BP];
     redirect = a.ctl[CTL_REDIRECT];
     u += (gen - 1) * m;
@@ -184,6 +187,10 @@ k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t nunits) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       const uint64_t keep = l2_policy_evict_last(), stream = l2_policy_evict_first();
+      const uint64_t plan_key = stream_key(a.plan.seed, kPlanStream0 + (uint64_t)gen);
+      int64_t* u_out = const_cast<int64_t*>(u);
+      int64_t* v_out = const_cast<int64_t*>(vv);
+      double* ms_out = const_cast<double*>(ms);
       int s = 0;
       uint32_t j = 0;
       // tickets are claimed kBatch units at a time, one claim ahead, so the
@@ -208,16 +215,32 @@ k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t nunits) {
         const int64_t t = unit / m, i = unit - t * m;
         const int64_t off = t * TILE;
         const int64_t n = min((int64_t)TILE, a.pitch - off);
-        const int64_t ui = u[i], vi = vv[i];
+        int64_t ui, vi;
+        double msd;
+        if (a.plan_inline) {
+          plan_slot(plan_key, i, a.plan.r, a.plan.ms_uniform, a.plan.ms_const, &ui, &vi, &msd);
+          if (t == 0 && a.write_plan) { u_out[i] = ui; v_out[i] = vi; ms_out[i] = msd; }
+        } else {
+          ui = u[i];
+          vi = vv[i];
+          msd = ms[i];
+        }
         const T* src = (i == redirect) ? elite_prev : S + i * a.pitch;
         const uint32_t bytes = (uint32_t)(n * sizeof(T));
         T* d = data + (int64_t)s * 3 * TILE;
         slot_unit[s] = unit;
+        slot_ms[s] = msd;
         mbar_expect_tx(full + s, 3 * bytes);
         bulk_g2s(d, src + off, bytes, full + s, stream);
         bulk_g2s(d + TILE, pool + ui * a.pitch + off, bytes, full + s, keep);
         bulk_g2s(d + 2 * TILE, pool + vi * a.pitch + off, bytes, full + s, keep);
         if (++s == kStages) { s = 0; ++j; }
+      }
+      // every claim of this CTA is done; the last CTA out re-arms the ticket
+      __threadfence();
+      if (atomicAdd(a.ticket + 1, 1ull) == (unsigned long long)gridDim.x - 1) {
+        atomicExch(a.ticket, 0ull);
+        atomicExch(a.ticket + 1, 0ull);
       }
     }
     return;
@@ -278,7 +301,7 @@ k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t nunits) {
       }
       cur_t = t;
     }
-    const T msv = (T)ms[i];
+    const T msv = (T)slot_ms[s];
     const bool save = (i == bp);
     const T* d = data + (int64_t)s * 3 * TILE;
     Vec P[VPT], A[VPT], B[VPT];
@@ -338,103 +361,7 @@ k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t nunits) {
 }
 
 constexpr size_t kTmaSmem = (size_t)kStages * 3 * kTileBytes + (size_t)kRedStages * kConsumerWarps * 2 * 8 +
-                            (2 * kStages + 2 * kRedStages) * 8 + (kStages + kRedStages) * 8;
-
-// ===================================================================
-// Plain-load variant kept only for A/B measurement (GSGP_GSM_LEGACY=1):
-// blockIdx -> (tile, group of kRowsPerBlock rows), 128-bit loads.
-// ===================================================================
-constexpr int kThreads = 256;
-constexpr int kRowsPerBlock = 8;
-
-template <typename T, bool kOp>
-__global__ void __launch_bounds__(kThreads, 2) k_gsm_plain(GsmArgs a, int64_t ntiles, int64_t ngroups) {
-  using Vec = typename Vec16<T>::type;
-  constexpr int EV = Vec16<T>::n;
-  constexpr int TILE = kTileBytes / (int)sizeof(T);
-  constexpr int V = TILE / (kThreads * EV);
-  constexpr int R = kRowsPerBlock;
-  __shared__ double red[kThreads / 32][R][2];
-  const int tid = threadIdx.x;
-  const int64_t tile = blockIdx.x / ngroups;
-  const int64_t i0 = (blockIdx.x - tile * ngroups) * R;
-  const int64_t* u = a.u;
-  const int64_t* vv = a.v;
-  const double* ms = a.ms;
-  int64_t bp = -1, redirect = -1;
-  const T* elite_prev = reinterpret_cast<const T*>(a.elite_prev);
-  T* elite_cur = reinterpret_cast<T*>(a.elite_cur);
-  if (a.ctl) {
-    const int64_t gen = a.ctl[CTL_GEN];
-    bp = a.ctl[CTL_BP];
-    redirect = a.ctl[CTL_REDIRECT];
-    u += (gen - 1) * a.m;
-    vv += (gen - 1) * a.m;
-    ms += (gen - 1) * a.m;
-    if (a.ctl[CTL_PARITY]) {
-      const T* t0 = elite_prev;
-      elite_prev = elite_cur;
-      elite_cur = const_cast<T*>(t0);
-    }
-  }
-  const T* pool = reinterpret_cast<const T*>(a.pool);
-  T* S = reinterpret_cast<T*>(a.S);
-  unsigned long long nonfinite = 0;
-  const int warp = tid >> 5, lane = tid & 31;
-  for (int r = 0; r < R; ++r) {
-    const int64_t i = i0 + r;
-    double acc_tr = 0.0, acc_te = 0.0;
-    if (i < a.m) {
-      const T msv = (T)ms[i];
-      const T* prow = (i == redirect) ? elite_prev : S + i * a.pitch;
-      const T* pu = pool + u[i] * a.pitch;
-      const T* pv = pool + vv[i] * a.pitch;
-#pragma unroll
-      for (int q = 0; q < V; ++q) {
-        const int64_t e = tile * TILE + (int64_t)(q * kThreads + tid) * EV;
-        if (e >= a.pitch) continue;
-        const Vec P = __ldcs(reinterpret_cast<const Vec*>(prow + e));
-        const Vec A = __ldg(reinterpret_cast<const Vec*>(pu + e));
-        const Vec B = __ldg(reinterpret_cast<const Vec*>(pv + e));
-        const T* pe = reinterpret_cast<const T*>(&P);
-        const T* ae = reinterpret_cast<const T*>(&A);
-        const T* be = reinterpret_cast<const T*>(&B);
-        Vec O;
-        T* oe = reinterpret_cast<T*>(&O);
-        double sacc = 0.0;
-        for (int c = 0; c < EV; ++c) {
-          T o = mut(pe[c], ae[c], be[c], msv, a.sign);
-          if (kOp && !isfinite((double)o)) { o = (T)0; ++nonfinite; }
-          oe[c] = o;
-          const double dd = __dsub_rn((double)o, __ldg(a.y + e + c));
-          sacc = __dadd_rn(sacc, __dmul_rn(dd, dd));
-        }
-        *reinterpret_cast<Vec*>(S + i * a.pitch + e) = O;
-        if (i == bp) *reinterpret_cast<Vec*>(elite_cur + e) = P;
-        if (e < a.test_off) acc_tr = __dadd_rn(acc_tr, sacc);
-        else acc_te = __dadd_rn(acc_te, sacc);
-      }
-    }
-    acc_tr = warp_sum(acc_tr);
-    acc_te = warp_sum(acc_te);
-    if (lane == 0) { red[warp][r][0] = acc_tr; red[warp][r][1] = acc_te; }
-  }
-  __syncthreads();
-  if (tid < 2 * R) {
-    const int r = tid >> 1, w2 = tid & 1;
-    const int64_t i = i0 + r;
-    if (i < a.m) {
-      double t = 0.0;
-      for (int w = 0; w < kThreads / 32; ++w) t = __dadd_rn(t, red[w][r][w2]);
-      a.part[(i * ntiles + tile) * 2 + w2] = t;
-    }
-  }
-  if (kOp) {
-    for (int o = 16; o > 0; o >>= 1) nonfinite += __shfl_xor_sync(0xffffffffu, nonfinite, o);
-    if (lane == 0 && nonfinite) atomicAdd(a.nonfinite, nonfinite);
-  }
-}
-
+                            (2 * kStages + 2 * kRedStages) * 8 + (2 * kStages + kRedStages) * 8;
 int g_num_sms = 0;
 
 }  // namespace
@@ -448,17 +375,6 @@ void launch_gsm(const GsmArgs& a, bool f64, bool operator_mode, cudaStream_t s) 
   if (a.m <= 0 || a.pitch <= 0) return;
   GSGP_REQUIRE(a.pitch % 32 == 0, "storage pitch must be a multiple of 32");
   const int64_t ntiles = gsm_tiles(a.pitch, f64);
-  static const bool legacy = getenv("GSGP_GSM_LEGACY") != nullptr;   // A/B measurement only
-  if (legacy) {
-    const int64_t ngroups = (a.m + kRowsPerBlock - 1) / kRowsPerBlock;
-    const int64_t blocks = ntiles * ngroups;
-    GSGP_REQUIRE(blocks < (1ll << 31), "generation grid too large");
-    auto go = [&](auto kern) { kern<<<(unsigned)blocks, kThreads, 0, s>>>(a, ntiles, ngroups); };
-    if (f64) operator_mode ? go(k_gsm_plain<double, true>) : go(k_gsm_plain<double, false>);
-    else operator_mode ? go(k_gsm_plain<float, true>) : go(k_gsm_plain<float, false>);
-    GSGP_CUDA(cudaGetLastError());
-    return;
-  }
   if (g_num_sms == 0) {
     int dev = 0;
     GSGP_CUDA(cudaGetDevice(&dev));
@@ -467,7 +383,6 @@ void launch_gsm(const GsmArgs& a, bool f64, bool operator_mode, cudaStream_t s) 
   const int64_t nunits = ntiles * a.m;
   const unsigned grid = (unsigned)std::min<int64_t>(g_num_sms, nunits);
   GSGP_REQUIRE(a.ticket != nullptr, "GSM launch needs a ticket counter");
-  GSGP_CUDA(cudaMemsetAsync(a.ticket, 0, sizeof(unsigned long long), s));
   auto go = [&](auto kern) {
     GSGP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
     kern<<<grid, kTmaThreads, kTmaSmem, s>>>(a, ntiles, nunits);

@@ -29,6 +29,24 @@ struct PlanParams {
   int32_t ms_uniform;
   double ms_const;
 };
+// slot i of a generation's plan (gsgp/mutation.py:37-62): counters 3i, 3i+1,
+// 3i+2 of stream 2^32+gen (key); u uniform over [0, r), v uniform over the
+// other r-1 indices, ms = 1 - U or the constant step.  All conversions are
+// the reference's fp64 product + truncation.
+#ifdef __CUDACC__
+__device__ __forceinline__ void plan_slot(uint64_t key, int64_t i, int64_t r, int32_t ms_uniform,
+                                          double ms_const, int64_t* pu, int64_t* pv, double* pms) {
+  const uint64_t c = 3ull * (uint64_t)i;
+  int64_t a = (int64_t)__dmul_rn(draw_unit(key, c), (double)r);
+  a = a < r - 1 ? a : r - 1;
+  int64_t b = (int64_t)__dmul_rn(draw_unit(key, c + 1), (double)(r - 1));
+  b = b < r - 2 ? b : r - 2;
+  b += (b >= a);
+  *pu = a;
+  *pv = b;
+  *pms = ms_uniform ? __dsub_rn(1.0, draw_unit(key, c + 2)) : ms_const;
+}
+#endif
 // plan for generation `gen` (explicit) or, when gen_ptr != nullptr, for
 // generation *gen_ptr read on device (graph-replayable)
 void launch_plan(const PlanParams& p, int64_t gen, const int64_t* gen_ptr, int64_t* u, int64_t* v,
@@ -91,7 +109,15 @@ struct GsmArgs {
   int32_t sign;             // 0 minus, 1 plus
   double* part;             // [m][ntiles][2]
   unsigned long long* nonfinite;   // operator mode only
-  unsigned long long* ticket;      // dynamic unit dispatch counter (zeroed per launch)
+  // {ticket, exited CTAs}: dynamic unit dispatch; zero before the first
+  // launch, the last CTA to exit re-zeroes both for the next launch
+  unsigned long long* ticket;
+  // inline mutation plan (gsgp/mutation.py:37-62): when plan_inline, the
+  // producer draws (u, v, ms) of each row itself from the counter RNG and,
+  // if write_plan, records them for the lineage into u/v/ms[(gen-1)*m + i]
+  int32_t plan_inline;
+  int32_t write_plan;
+  PlanParams plan;
 };
 int64_t gsm_tiles(int64_t pitch, bool f64);
 void launch_gsm(const GsmArgs& a, bool f64, bool operator_mode, cudaStream_t s);
@@ -121,6 +147,10 @@ struct SurviveArgs {
   double* trace_tr; double* trace_te;
 };
 void launch_survive(const SurviveArgs& a, cudaStream_t s);
+// per-row SSE tile reduction into sse (== a.sse_off) fused with survival
+// (single shard, single rank); `done` is a zeroed counter, re-zeroed on exit
+void launch_reduce_survive(const double* part, int64_t ntiles, double* sse, const SurviveArgs& a,
+                           unsigned int* done, cudaStream_t s);
 // initial elite: fitness from SSE, argmin, trace[0] (evolution.py:132-143)
 void launch_init_state(const SurviveArgs& a, cudaStream_t s);
 // decision only, for the operator API: out = {src, idx, slot}

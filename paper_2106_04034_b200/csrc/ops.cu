@@ -69,17 +69,8 @@ __global__ void k_plan(PlanParams p, int64_t gen, const int64_t* gen_ptr, int64_
   if (i >= p.m) return;
   int64_t g = gen_ptr ? gen_ptr[CTL_GEN] : gen;
   int64_t off = gen_ptr ? (g - 1) * stride : 0;
-  uint64_t key = stream_key(p.seed, kPlanStream0 + (uint64_t)g);
-  uint64_t c = 3ull * (uint64_t)i;
-  double du = draw_unit(key, c), dv = draw_unit(key, c + 1);
-  int64_t a = (int64_t)__dmul_rn(du, (double)p.r);
-  a = a < p.r - 1 ? a : p.r - 1;
-  int64_t b = (int64_t)__dmul_rn(dv, (double)(p.r - 1));
-  b = b < p.r - 2 ? b : p.r - 2;
-  b += (b >= a);
-  u[off + i] = a;
-  v[off + i] = b;
-  ms[off + i] = p.ms_uniform ? __dsub_rn(1.0, draw_unit(key, c + 2)) : p.ms_const;
+  const uint64_t key = stream_key(p.seed, kPlanStream0 + (uint64_t)g);
+  plan_slot(key, i, p.r, p.ms_uniform, p.ms_const, u + off + i, v + off + i, ms + off + i);
 }
 
 // ------------------------------------------------------- reductions
@@ -189,9 +180,12 @@ constexpr ArgVal kMaxInit{-INFINITY, INT64_MAX};
 // gsgp/evolution.py:65-83 plus the loop bookkeeping at :146-158.
 // Slot flags (wide): a slot whose semantics overflowed fp32 at
 // initialisation keeps its (constant) fp64 fitness — see DESIGN.md §4.
-__global__ void __launch_bounds__(1024) k_survive(SurviveArgs a) {
-  __shared__ ArgVal sh[32];
-  __shared__ int64_t dec[4];
+// One block of any size: the three arg-reductions share one shared-memory
+// exchange, and the next generation's best parent needs no pass at all
+// (it is the elite slot: a parent elite is strictly below every offspring,
+// an offspring elite is the offspring minimum).
+__device__ void survive_block(const SurviveArgs& a) {
+  __shared__ ArgVal sh[3][32];
   const int64_t m = a.m;
   ArgVal bp = kMinInit, bo = kMinInit, wo = kMaxInit;
   for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
@@ -204,10 +198,25 @@ __global__ void __launch_bounds__(1024) k_survive(SurviveArgs a) {
     bo = better_min(bo, ArgVal{fo, i});
     wo = better_max(wo, ArgVal{fo, i});
   }
-  bp = block_arg<true>(bp, sh);
-  bo = block_arg<true>(bo, sh);
-  wo = block_arg<false>(wo, sh);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ArgVal x{__shfl_xor_sync(0xffffffffu, bp.v, o), __shfl_xor_sync(0xffffffffu, bp.i, o)};
+    ArgVal y{__shfl_xor_sync(0xffffffffu, bo.v, o), __shfl_xor_sync(0xffffffffu, bo.i, o)};
+    ArgVal z{__shfl_xor_sync(0xffffffffu, wo.v, o), __shfl_xor_sync(0xffffffffu, wo.i, o)};
+    bp = better_min(bp, x);
+    bo = better_min(bo, y);
+    wo = better_max(wo, z);
+  }
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if ((threadIdx.x & 31) == 0) { sh[0][w] = bp; sh[1][w] = bo; sh[2][w] = wo; }
+  __syncthreads();
   if (threadIdx.x == 0) {
+    bp = sh[0][0]; bo = sh[1][0]; wo = sh[2][0];
+    for (int k = 1; k < nw; ++k) {
+      bp = better_min(bp, sh[0][k]);
+      bo = better_min(bo, sh[1][k]);
+      wo = better_max(wo, sh[2][k]);
+    }
     int64_t g = a.ctl[CTL_GEN];
     int8_t src;
     int64_t idx, slot;
@@ -231,22 +240,46 @@ __global__ void __launch_bounds__(1024) k_survive(SurviveArgs a) {
     a.rec_fit[g] = fit;
     a.trace_tr[g] = fit;
     a.trace_te[g] = rmse_of(a.To[slot], a.nte);
-    dec[0] = slot;
-  }
-  __syncthreads();
-  ArgVal nb = kMinInit;
-  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
-    double f = a.Fo[i];
-    a.F[i] = f;
-    a.TS[i] = a.To[i];
-    nb = better_min(nb, ArgVal{f, i});
-  }
-  nb = block_arg<true>(nb, sh);
-  if (threadIdx.x == 0) {
-    a.ctl[CTL_BP] = nb.i;
+    a.ctl[CTL_BP] = slot;          // argmin of the surviving fitness vector
     a.ctl[CTL_PARITY] ^= 1;
     a.ctl[CTL_GEN] += 1;
   }
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+    a.F[i] = a.Fo[i];
+    a.TS[i] = a.To[i];
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_survive(SurviveArgs a) { survive_block(a); }
+
+// SSE tile reduction of every row (one block per row, fixed order) fused
+// with survival: the last block to finish runs survive_block.
+__global__ void __launch_bounds__(256) k_reduce_survive(const double* __restrict__ part, int64_t ntiles,
+                                                        double* __restrict__ sse, SurviveArgs a,
+                                                        unsigned int* done) {
+  __shared__ double sh[32];
+  __shared__ int last;
+  const int64_t row = blockIdx.x;
+  const double* p = part + row * ntiles * 2;
+  double x = 0.0, z = 0.0;
+  for (int64_t t = threadIdx.x; t < ntiles; t += blockDim.x) {
+    x = __dadd_rn(x, p[2 * t]);
+    z = __dadd_rn(z, p[2 * t + 1]);
+  }
+  x = block_sum(x, sh);
+  z = block_sum(z, sh);
+  if (threadIdx.x == 0) {
+    sse[2 * row] = x;
+    sse[2 * row + 1] = z;
+    __threadfence();
+    last = atomicAdd(done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  survive_block(a);
+  if (threadIdx.x == 0) *done = 0;
 }
 
 // evolution.py:132-143: initial fitness, elite and trace[0]
@@ -364,6 +397,12 @@ void launch_row_rmse(const double* S, const double* y, int64_t m, int64_t n, dou
                      cudaStream_t s) {
   if (m <= 0) return;
   k_row_rmse<<<(unsigned)m, 256, 0, s>>>(S, y, n, out);
+  check_launch();
+}
+
+void launch_reduce_survive(const double* part, int64_t ntiles, double* sse, const SurviveArgs& a,
+                           unsigned int* done, cudaStream_t s) {
+  k_reduce_survive<<<(unsigned)a.m, 256, 0, s>>>(part, ntiles, sse, a, done);
   check_launch();
 }
 
