@@ -84,12 +84,18 @@ struct __align__(16) Ins {
   uint8_t op;    // InsOp
   uint8_t ls;    // InsSrc of the left operand (or the LOAD source)
   uint8_t rs;    // InsSrc of the right operand
-  uint8_t pad;
+  uint8_t kind;  // dispatch key: op*16 + ls*4 + rs; LOAD: 64 + ls; PUSH: 80
   uint16_t lf;   // feature index when ls == SRC_FEAT
   uint16_t rf;   // feature index when rs == SRC_FEAT
   double c;      // constant when ls or rs == SRC_CONST (never both)
 };
 static_assert(sizeof(Ins) == 16, "Ins must be 16 bytes");
+constexpr int kKindLoad = 64, kKindPush = 80;
+__host__ __device__ __forceinline__ uint8_t ins_kind(const Ins& in) {
+  if (in.op == INS_PUSH) return kKindPush;
+  if (in.op == INS_LOAD) return (uint8_t)(kKindLoad + in.ls);
+  return (uint8_t)(in.op * 16 + in.ls * 4 + in.rs);
+}
 
 // binary op with the reference's protected division (interpreter.py:58-65):
 // each case rounds exactly once, as numpy does.

@@ -91,6 +91,7 @@ __global__ void k_compile(const uint8_t* __restrict__ tags, const int32_t* __res
     in.op = INS_LOAD;
     if (root < 0) { in.ls = SRC_CONST; in.c = 0.0; }
     else leaf_src(root, in.ls, in.lf, in.c);
+    in.kind = ins_kind(in);
     out[pc++] = in;
   } else {
     depth = fl[root] & F_NEED;
@@ -113,6 +114,7 @@ __global__ void k_compile(const uint8_t* __restrict__ tags, const int32_t* __res
       if (st == 1 && both) {
         Ins p{};
         p.op = INS_PUSH;
+        p.kind = ins_kind(p);
         out[pc++] = p;
         work[top - 1] = n * 4 + 2;
         work[top++] = second * 4;
@@ -133,6 +135,7 @@ __global__ void k_compile(const uint8_t* __restrict__ tags, const int32_t* __res
         leaf_src(l, in.ls, in.lf, in.c);
         in.rs = SRC_ACC;
       }
+      in.kind = ins_kind(in);
       out[pc++] = in;
       --top;
     }
@@ -141,6 +144,57 @@ __global__ void k_compile(const uint8_t* __restrict__ tags, const int32_t* __res
   P.depth[g] = depth;
   atomicMax(P.maxdepth, depth);
 }
+
+// Per-thread evaluation state for CPT cases, with one fully specialised body
+// per instruction kind (operator x left source x right source).
+template <int CPT, bool kXSmem>
+struct Frame {
+  static constexpr int B = 128, TILE = B * CPT;
+  double (&acc)[CPT];
+  double* stack;               // [depth][TILE] spill stack
+  const double* xs;            // [l][TILE] feature tile (kXSmem)
+  const double* XT;            // [l][xt_pitch] features in global memory (!kXSmem)
+  int64_t xt_pitch, q0;
+  const bool (&valid)[CPT];
+  int tid;
+  double eps;
+
+  template <int S>
+  __device__ __forceinline__ double get(int c, int sp, int f, double cst) const {
+    const int cc = c * B + tid;
+    if constexpr (S == SRC_ACC) return acc[c];
+    else if constexpr (S == SRC_POP) return stack[sp * TILE + cc];
+    else if constexpr (S == SRC_FEAT) {
+      if constexpr (kXSmem) return xs[f * TILE + cc];
+      else return valid[c] ? XT[f * xt_pitch + q0 + cc] : 0.0;
+    } else return cst;
+  }
+  // the reference's binary op, one IEEE rounding per case (interpreter.py:58-65)
+  template <int OP, int LS, int RS>
+  __device__ __forceinline__ void op(int& sp, int lf, int rf, double cst) {
+    if constexpr (LS == SRC_POP || RS == SRC_POP) --sp;
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      const double l = get<LS>(c, sp, lf, cst), r = get<RS>(c, sp, rf, cst);
+      double v;
+      if constexpr (OP == OP_ADD) v = __dadd_rn(l, r);
+      else if constexpr (OP == OP_SUB) v = __dsub_rn(l, r);
+      else if constexpr (OP == OP_MUL) v = __dmul_rn(l, r);
+      else v = fabs(r) < eps ? 1.0 : __ddiv_rn(l, r);
+      acc[c] = v;
+    }
+  }
+  template <int S>
+  __device__ __forceinline__ void load(int& sp, int f, double cst) {
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) acc[c] = get<S>(c, sp, f, cst);
+  }
+  __device__ __forceinline__ void push(int& sp) {
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) stack[sp * TILE + c * B + tid] = acc[c];
+    ++sp;
+  }
+};
 
 template <int CPT, int MODE, typename TOut, bool kXSmem>
 __global__ void __launch_bounds__(128) k_interpret(InterpArgs a, int64_t ntiles, int64_t gpb) {
@@ -185,38 +239,35 @@ __global__ void __launch_bounds__(128) k_interpret(InterpArgs a, int64_t ntiles,
 #pragma unroll
     for (int c = 0; c < CPT; ++c) acc[c] = 0.0;
     int sp = 0;
+    Frame<CPT, kXSmem> fr{acc, stack, xs, a.XT, a.xt_pitch, q0, valid, tid, a.eps};
+    uint4 nxt = len > 0 ? __ldg(code) : make_uint4(0, 0, 0, 0);
     for (int i = 0; i < len; ++i) {
-      uint4 raw = __ldg(code + i);
-      const int op = raw.x & 0xff, ls = (raw.x >> 8) & 0xff, rs = (raw.x >> 16) & 0xff;
+      const uint4 raw = nxt;
+      if (i + 1 < len) nxt = __ldg(code + i + 1);   // prefetch the next instruction
+      const int kind = raw.x >> 24;
       const int lf = raw.y & 0xffff, rf = raw.y >> 16;
       const double cst = __hiloint2double((int)raw.w, (int)raw.z);
-      if (op == INS_PUSH) {
-#pragma unroll
-        for (int c = 0; c < CPT; ++c) stack[(int64_t)sp * TILE + c * B + tid] = acc[c];
-        ++sp;
-        continue;
-      }
-      if (ls == SRC_POP || rs == SRC_POP) --sp;
-#pragma unroll
-      for (int c = 0; c < CPT; ++c) {
-        const int64_t cc = c * B + tid;
-        double lv, rv;
-        switch (ls) {
-          case SRC_ACC: lv = acc[c]; break;
-          case SRC_POP: lv = stack[(int64_t)sp * TILE + cc]; break;
-          case SRC_FEAT: lv = kXSmem ? xs[(int64_t)lf * TILE + cc]
-                                     : (valid[c] ? a.XT[lf * a.xt_pitch + q0 + cc] : 0.0); break;
-          default: lv = cst;
-        }
-        if (op == INS_LOAD) { acc[c] = lv; continue; }
-        switch (rs) {
-          case SRC_ACC: rv = acc[c]; break;
-          case SRC_POP: rv = stack[(int64_t)sp * TILE + cc]; break;
-          case SRC_FEAT: rv = kXSmem ? xs[(int64_t)rf * TILE + cc]
-                                     : (valid[c] ? a.XT[rf * a.xt_pitch + q0 + cc] : 0.0); break;
-          default: rv = cst;
-        }
-        acc[c] = apply_op(op, lv, rv, a.eps);
+      // one warp-uniform indirect branch per instruction; every case body is
+      // straight-line code over the CPT cases of this thread
+      switch (kind) {
+#define GSGP_K(OP, LS, RS) \
+  case OP * 16 + LS * 4 + RS: fr.template op<OP, LS, RS>(sp, lf, rf, cst); break;
+#define GSGP_K4(LS, RS) GSGP_K(0, LS, RS) GSGP_K(1, LS, RS) GSGP_K(2, LS, RS) GSGP_K(3, LS, RS)
+        GSGP_K4(SRC_ACC, SRC_POP)
+        GSGP_K4(SRC_POP, SRC_ACC)
+        GSGP_K4(SRC_ACC, SRC_FEAT)
+        GSGP_K4(SRC_ACC, SRC_CONST)
+        GSGP_K4(SRC_FEAT, SRC_ACC)
+        GSGP_K4(SRC_CONST, SRC_ACC)
+        GSGP_K4(SRC_FEAT, SRC_FEAT)
+        GSGP_K4(SRC_FEAT, SRC_CONST)
+        GSGP_K4(SRC_CONST, SRC_FEAT)
+#undef GSGP_K4
+#undef GSGP_K
+        case kKindLoad + SRC_FEAT: fr.template load<SRC_FEAT>(sp, lf, cst); break;
+        case kKindLoad + SRC_CONST: fr.template load<SRC_CONST>(sp, lf, cst); break;
+        case kKindPush: fr.push(sp); break;
+        default: __trap();   // the compiler never emits any other kind
       }
     }
     // ---- epilogue: non-finite -> 0.0 counted (core.py:348-356), then store
