@@ -56,28 +56,39 @@ def init_state(s_pop_tr, s_pop_te, ytr, yte):
     return P_tr, P_te, F, TS, wide.astype(np.int32)
 
 
-def run32(cfg: R.Cfg, Xtr, ytr, Xte, yte, shard_sse=None):
-    """The engine's run in fp32 storage.  `shard_sse(S_tr, S_te)` may replace
-    the local SSE with an exchanged (e.g. allreduced) one for sharding tests;
-    it receives/returns (sse_train[m], sse_test[m])."""
+def run32(cfg: R.Cfg, Xtr, ytr, Xte, yte, exchange=None, n_total=None):
+    """The engine's run in fp32 storage.
+
+    Sharded use (the multi-GPU protocol): each caller passes only
+    its case slice, `n_total=(n_train, n_test)` of the whole dataset, and
+    `exchange(name, array) -> array` summing an array over all shards (the
+    NCCL allreduce of the engine).  Exchanged: per-row SSE (init and every
+    generation), the fp32-overflow flags and the non-finite count."""
     m, r, g, l = cfg.m, cfg.r, cfg.g, Xtr.shape[1]
     kw = dict(p_function=cfg.p[0], p_feature=cfg.p[1], p_constant=cfg.p[2],
               erc_low=cfg.erc[0], erc_high=cfg.erc[1])
     pop = R.genomes(m, cfg.k, l, cfg.seed, 0, **kw)
     trees = R.genomes(r, cfg.k, l, cfg.seed, m, **kw)
     stacked = np.vstack([Xtr, Xte])
-    ntr, nte = Xtr.shape[0], Xte.shape[0]
+    ntr_l, nte_l = Xtr.shape[0], Xte.shape[0]
+    ntr, nte = n_total if n_total else (ntr_l, nte_l)
+    xch = exchange or (lambda name, arr: arr)
     s_pop, c1 = R.semantics(*pop, stacked, cfg.eps)
     s_tree, c2 = R.semantics(*trees, stacked, cfg.eps)
-    P_tr, P_te, F, TS, wide = init_state(s_pop[:, :ntr], s_pop[:, ntr:], ytr, yte)
-    if shard_sse is not None:
-        a, b = shard_sse(sse(s_pop[:, :ntr], ytr), sse(s_pop[:, ntr:], yte))
-        F, TS = rmse_from_sse(a, ntr), b
+    with np.errstate(over="ignore"):
+        P_tr = s_pop[:, :ntr_l].astype(np.float32)
+        P_te = s_pop[:, ntr_l:].astype(np.float32)
+    bits = np.stack([np.isinf(P_tr).any(axis=1), np.isinf(P_te).any(axis=1)], axis=1).astype(np.int64)
+    bits = xch("wide", bits)
+    wide = ((bits[:, 0] > 0) * 1 | (bits[:, 1] > 0) * 2).astype(np.int32)
+    s0 = xch("sse", np.stack([sse(s_pop[:, :ntr_l], ytr), sse(s_pop[:, ntr_l:], yte)], axis=1))
+    F, TS = rmse_from_sse(s0[:, 0], ntr), s0[:, 1].copy()
+    overflow = int(xch("overflow", np.array([c1 + c2], np.int64))[0])
     Q = R.sigmoid(s_tree).astype(np.float32)
-    Q_tr, Q_te = Q[:, :ntr], Q[:, ntr:]
+    Q_tr, Q_te = Q[:, :ntr_l], Q[:, ntr_l:]
     b0 = int(np.argmin(F))
     out = {"train": np.empty(g + 1), "test": np.empty(g + 1), "elite": [],
-           "initial": ("initial", b0, b0, float(F[b0])), "overflow": c1 + c2,
+           "initial": ("initial", b0, b0, float(F[b0])), "overflow": overflow,
            "u": np.empty((g, m), np.int64), "v": np.empty((g, m), np.int64), "ms": np.empty((g, m))}
     out["train"][0] = F[b0]
     out["test"][0] = rmse_from_sse(TS[b0], nte)
@@ -85,9 +96,8 @@ def run32(cfg: R.Cfg, Xtr, ytr, Xte, yte, shard_sse=None):
         u, v, ms = R.plan(m, r, cfg.seed, gen, cfg.mutation_step)
         O_tr = gsm_step32(P_tr, Q_tr, u, v, ms, cfg.sign)
         O_te = gsm_step32(P_te, Q_te, u, v, ms, cfg.sign)
-        s_tr, s_te = sse(O_tr, ytr), sse(O_te, yte)
-        if shard_sse is not None:
-            s_tr, s_te = shard_sse(s_tr, s_te)
+        s = xch("sse", np.stack([sse(O_tr, ytr), sse(O_te, yte)], axis=1))
+        s_tr, s_te = s[:, 0], s[:, 1]
         Fo = np.where(wide & 1, F, rmse_from_sse(s_tr, ntr))
         To = np.where(wide & 2, TS, s_te)
         src, idx, slot = R.survive(F, Fo)
