@@ -216,6 +216,24 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_leg(c, args.cpu_budget)
 
+    # secondary single-GPU line on C2 (configs[1]) for context, same method
+    secondary = None
+    if world == 1 and args.config == "c3" and not args.no_secondary:
+        c2 = CONFIGS["c2"]
+        tr2 = G.make_benchmark_dataset(c2["ntr"], c2["l"], seed=1)
+        te2 = G.make_benchmark_dataset(c2["nte"], c2["l"], seed=2)
+        K2 = 500
+        r2 = G.run_evolution(G.RunConfig(population_size=c2["m"], random_trees=c2["r"],
+                                         program_size=c2["k"], generations=W + K2, seed=1),
+                             tr2, te2, time_kernels=True, window_start=W)
+        b2 = bytes_per_generation([(e.plan.u, e.plan.v) for e in r2.lineage.entries[W:]],
+                                  c2["ntr"] + c2["nte"], c2["m"])
+        a2 = float(b2.sum() / (r2.device["window_gsm_ms"] / 1e3) / 1e9)
+        secondary = {"workload": c2["desc"], "steps": K2,
+                     "value": K2 / (r2.device["window_ms"] / 1e3), "unit": "generations/s",
+                     "roofline": {"achieved": a2, "peak": peak, "unit": "GB/s", "frac": a2 / peak,
+                                  "kernel_share_of_step": r2.device["window_gsm_ms"] / r2.device["window_ms"]}}
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "generations/s", "n_gpus": world,
@@ -241,7 +259,10 @@ def run_ours(args):
             "clocks": clocks,
             "init_ms": {"create_population": res.timings.create_population_ms,
                         "compute_semantics": res.timings.compute_semantics_ms},
-            "graph_mode_note": "timed run uses direct launches with per-kernel events",
+            "timing_note": "timed run: direct launches with CUDA events around every GSM launch "
+                           "on the engine stream (run_evolution(time_kernels=True)); the default "
+                           "API path replays one captured generation as a CUDA graph",
+            "secondary": secondary,
         }
         print(json.dumps(line))
     if world > 1:
@@ -303,6 +324,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--no-secondary", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -90,26 +90,23 @@ __device__ double block_sum(double v, double* sh) {
 
 // part[row][tile][2] -> out[row][2]; tiles are summed per thread in index
 // order, then combined by a fixed tree: a function of case positions only.
-__global__ void k_reduce_partials(const double* __restrict__ part, int64_t ntiles,
-                                  double* __restrict__ out, int accumulate) {
-  __shared__ double sh[32];
-  int64_t row = blockIdx.x;
+// One warp per row (same order as the fused k_reduce_survive below).
+__global__ void k_reduce_partials(const double* __restrict__ part, int64_t ntiles, int64_t rows,
+                                  double* __restrict__ out) {
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const int lane = threadIdx.x & 31;
   const double* p = part + row * ntiles * 2;
   double a = 0.0, b = 0.0;
-  for (int64_t t = threadIdx.x; t < ntiles; t += blockDim.x) {
+  for (int64_t t = lane; t < ntiles; t += 32) {
     a = __dadd_rn(a, p[2 * t]);
     b = __dadd_rn(b, p[2 * t + 1]);
   }
-  a = block_sum(a, sh);
-  b = block_sum(b, sh);
-  if (threadIdx.x == 0) {
-    if (accumulate) {
-      out[2 * row] = __dadd_rn(out[2 * row], a);
-      out[2 * row + 1] = __dadd_rn(out[2 * row + 1], b);
-    } else {
-      out[2 * row] = a;
-      out[2 * row + 1] = b;
-    }
+  a = warp_sum(a);
+  b = warp_sum(b);
+  if (lane == 0) {
+    out[2 * row] = a;
+    out[2 * row + 1] = b;
   }
 }
 
@@ -255,26 +252,35 @@ __global__ void __launch_bounds__(1024) k_survive(SurviveArgs a) { survive_block
 
 // SSE tile reduction of every row (one block per row, fixed order) fused
 // with survival: the last block to finish runs survive_block.
+// One warp per row: lane l sums tiles l, l+32, ... in order, then a fixed
+// butterfly — one wave of blocks, no block barriers on the reduction path.
+__device__ __forceinline__ void warp_row_sse(const double* __restrict__ part, int64_t ntiles,
+                                             int64_t row, double* __restrict__ sse) {
+  const int lane = threadIdx.x & 31;
+  const double* p = part + row * ntiles * 2;
+  double x = 0.0, z = 0.0;
+  for (int64_t t = lane; t < ntiles; t += 32) {
+    const double2 v = *reinterpret_cast<const double2*>(p + 2 * t);
+    x = __dadd_rn(x, v.x);
+    z = __dadd_rn(z, v.y);
+  }
+  x = warp_sum(x);
+  z = warp_sum(z);
+  if (lane == 0) {
+    sse[2 * row] = x;
+    sse[2 * row + 1] = z;
+  }
+}
+
 __global__ void __launch_bounds__(256) k_reduce_survive(const double* __restrict__ part, int64_t ntiles,
                                                         double* __restrict__ sse, SurviveArgs a,
                                                         unsigned int* done) {
-  __shared__ double sh[32];
   __shared__ int last;
-  const int64_t row = blockIdx.x;
-  const double* p = part + row * ntiles * 2;
-  double x = 0.0, z = 0.0;
-  for (int64_t t = threadIdx.x; t < ntiles; t += blockDim.x) {
-    x = __dadd_rn(x, p[2 * t]);
-    z = __dadd_rn(z, p[2 * t + 1]);
-  }
-  x = block_sum(x, sh);
-  z = block_sum(z, sh);
-  if (threadIdx.x == 0) {
-    sse[2 * row] = x;
-    sse[2 * row + 1] = z;
-    __threadfence();
-    last = atomicAdd(done, 1u) == gridDim.x - 1;
-  }
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row < a.m) warp_row_sse(part, ntiles, row, sse);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
   __syncthreads();
   if (!last) return;
   __threadfence();
@@ -381,7 +387,8 @@ void launch_plan(const PlanParams& p, int64_t gen, const int64_t* gen_ptr, int64
 void launch_reduce_partials(const double* part, int64_t rows, int64_t ntiles, double* out,
                             bool accumulate, cudaStream_t s) {
   if (rows <= 0) return;
-  k_reduce_partials<<<(unsigned)rows, 128, 0, s>>>(part, ntiles, out, accumulate ? 1 : 0);
+  GSGP_REQUIRE(!accumulate, "accumulating partial reduction is not supported");
+  k_reduce_partials<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(part, ntiles, rows, out);
   check_launch();
 }
 
@@ -402,7 +409,7 @@ void launch_row_rmse(const double* S, const double* y, int64_t m, int64_t n, dou
 
 void launch_reduce_survive(const double* part, int64_t ntiles, double* sse, const SurviveArgs& a,
                            unsigned int* done, cudaStream_t s) {
-  k_reduce_survive<<<(unsigned)a.m, 256, 0, s>>>(part, ntiles, sse, a, done);
+  k_reduce_survive<<<(unsigned)((a.m + 7) / 8), 256, 0, s>>>(part, ntiles, sse, a, done);
   check_launch();
 }
 
