@@ -85,7 +85,9 @@ class ClockSampler(threading.Thread):
                 N.nvmlDeviceGetCurrentClocksThrottleReasons
             while not self.stop_flag.is_set():
                 util = N.nvmlDeviceGetUtilizationRates(h).gpu
-                self.samples.append((N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM), int(get_reasons(h)), util))
+                self.samples.append((N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM), int(get_reasons(h)), util,
+                                     N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_MEM),
+                                     N.nvmlDeviceGetPowerUsage(h) / 1000.0, time.perf_counter()))
                 time.sleep(self.period)
         except Exception as exc:  # no NVML: report what we have
             self.ok = False
@@ -96,12 +98,14 @@ class ClockSampler(threading.Thread):
         self.join(timeout=2)
         load = [s for s in self.samples if s[2] >= 30] or self.samples
         reasons = set()
-        for _, bits, _ in load:
+        for s in load:
             for bit, name in NVML_REASONS.items():
-                if bits & bit and name != "gpu_idle":
+                if s[1] & bit and name != "gpu_idle":
                     reasons.add(name)
-        return {"sm_mhz": statistics.median([s[0] for s in load]) if load else None,
-                "sm_max_mhz": self.max_mhz, "reasons": sorted(reasons),
+        med = lambda k: statistics.median([s[k] for s in load]) if load else None  # noqa: E731
+        return {"sm_mhz": med(0), "sm_max_mhz": self.max_mhz, "reasons": sorted(reasons),
+                "mem_mhz": med(3), "power_w_median": med(4),
+                "power_w_max": max((s[4] for s in load), default=None),
                 "samples": len(self.samples), "samples_under_load": len(load)}
 
 

@@ -65,6 +65,7 @@ typedef struct gsgp_outputs {
   int64_t* plan_v;               /* [g][m] or NULL */
   double* plan_ms;               /* [g][m] or NULL */
   double* elite_train_semantics; /* [n_train]; this rank's case slice is filled */
+  double* gsm_ms;                /* [g] per-generation GSM kernel ms (time_kernels) or NULL */
   int64_t overflow;              /* out: non-finite replacements (RunStats) */
   int64_t shard_train_lo;        /* out: this rank's train case slice */
   int64_t shard_train_hi;

@@ -52,6 +52,7 @@ class GsgpOutputs(C.Structure):
         ("elite_fit", C.c_void_p),
         ("plan_u", C.c_void_p), ("plan_v", C.c_void_p), ("plan_ms", C.c_void_p),
         ("elite_train_semantics", C.c_void_p),
+        ("gsm_ms", C.c_void_p),
         ("overflow", C.c_int64),
         ("shard_train_lo", C.c_int64), ("shard_train_hi", C.c_int64),
         ("stage_ms", C.c_double * 12),

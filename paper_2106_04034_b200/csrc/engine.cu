@@ -481,6 +481,7 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   if (timed)
     for (int64_t t = 0; t < g; ++t) {
       const double d = elapsed_ms(*tev[2 * t], *tev[2 * t + 1]);
+      if (out->gsm_ms) out->gsm_ms[t] = d;
       gsm_ms += d;
       if (t >= w0) win_gsm_ms += d;
     }

@@ -68,7 +68,7 @@ constexpr int kTileBytes = 16384;
 // ===================================================================
 constexpr int kStages = 4;
 constexpr int kRedStages = 4;
-constexpr int kConsumerWarps = 8;
+constexpr int kConsumerWarps = 16;
 constexpr int kNCT = kConsumerWarps * 32;
 constexpr int kTmaThreads = (kConsumerWarps + 2) * 32;
 
@@ -334,7 +334,7 @@ k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t nunits) {
         if (kOp && !isfinite((double)o)) { o = (T)0; ++nonfinite; }
         oe[c] = o;
         const double dd = __dsub_rn((double)o, y[q][c]);
-        sacc = __dadd_rn(sacc, __dmul_rn(dd, dd));
+        sacc = __fma_rn(dd, dd, sacc);   // one fused op: fewer fp64 issues (power-bound)
       }
       __stcs(reinterpret_cast<Vec*>(orow + e), O);
       if (save) __stcs(reinterpret_cast<Vec*>(elite_cur + off + e), P[q]);

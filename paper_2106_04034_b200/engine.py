@@ -97,6 +97,7 @@ def run_evolution(cfg: RunConfig, train: Dataset, test: Dataset, *, storage: str
         elite_slot=np.empty(g + 1, np.int64), elite_fit=np.empty(g + 1),
         plan_u=np.empty((max(g, 1), m), np.int64), plan_v=np.empty((max(g, 1), m), np.int64),
         plan_ms=np.empty((max(g, 1), m)), elite_train_semantics=np.zeros(train.n_cases),
+        gsm_ms=np.zeros(max(g, 1)),
     )
     for name, arr in arrays.items():
         setattr(out, name, ptr(arr))
@@ -118,6 +119,7 @@ def run_evolution(cfg: RunConfig, train: Dataset, test: Dataset, *, storage: str
               "loop_launches": int(st[7]), "engine_total_ms": st[4],
               "window_ms": st[8], "window_gsm_ms": st[9], "window_gsm_launches": int(st[10]),
               "window_loop_launches": int(st[11]),
+              "gsm_ms_per_generation": a["gsm_ms"][:g] if time_kernels else None,
               "shard_train_range": (int(out.shard_train_lo), int(out.shard_train_hi)),
               "storage": storage}
     return RunResult(
