@@ -56,7 +56,7 @@ def init_state(s_pop_tr, s_pop_te, ytr, yte):
     return P_tr, P_te, F, TS, wide.astype(np.int32)
 
 
-def run32(cfg: R.Cfg, Xtr, ytr, Xte, yte, exchange=None, n_total=None):
+def run32(cfg: R.Cfg, Xtr, ytr, Xte, yte, exchange=None, n_total=None, wide_slots=True):
     """The engine's run in fp32 storage.
 
     Sharded use (the multi-GPU protocol): each caller passes only
@@ -81,14 +81,21 @@ def run32(cfg: R.Cfg, Xtr, ytr, Xte, yte, exchange=None, n_total=None):
     bits = np.stack([np.isinf(P_tr).any(axis=1), np.isinf(P_te).any(axis=1)], axis=1).astype(np.int64)
     bits = xch("wide", bits)
     wide = ((bits[:, 0] > 0) * 1 | (bits[:, 1] > 0) * 2).astype(np.int32)
-    s0 = xch("sse", np.stack([sse(s_pop[:, :ntr_l], ytr), sse(s_pop[:, ntr_l:], yte)], axis=1))
-    F, TS = rmse_from_sse(s0[:, 0], ntr), s0[:, 1].copy()
+    if not wide_slots:          # negative control: plain fp32 storage semantics
+        wide[:] = 0
+    # initial fitness from the STORED (fp32) semantics — the same values and
+    # order a generation uses, so an offspring equal to its parent ties with
+    # it exactly — except fp32-overflow slots, which keep the fp64 SSE
+    s_st = xch("sse", np.stack([sse(P_tr, ytr), sse(P_te, yte)], axis=1))
+    s64 = xch("sse", np.stack([sse(s_pop[:, :ntr_l], ytr), sse(s_pop[:, ntr_l:], yte)], axis=1))
+    F = np.where(wide & 1, rmse_from_sse(s64[:, 0], ntr), rmse_from_sse(s_st[:, 0], ntr))
+    TS = np.where(wide & 2, s64[:, 1], s_st[:, 1])
     overflow = int(xch("overflow", np.array([c1 + c2], np.int64))[0])
     Q = R.sigmoid(s_tree).astype(np.float32)
     Q_tr, Q_te = Q[:, :ntr_l], Q[:, ntr_l:]
     b0 = int(np.argmin(F))
     out = {"train": np.empty(g + 1), "test": np.empty(g + 1), "elite": [],
-           "initial": ("initial", b0, b0, float(F[b0])), "overflow": overflow,
+           "initial": ("initial", b0, b0, float(F[b0])), "overflow": overflow, "wide0": wide.copy(),
            "u": np.empty((g, m), np.int64), "v": np.empty((g, m), np.int64), "ms": np.empty((g, m))}
     out["train"][0] = F[b0]
     out["test"][0] = rmse_from_sse(TS[b0], nte)

@@ -167,7 +167,7 @@ inline unsigned nblk(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t
 struct Shard {
   int64_t tr_lo = 0, tr_hi = 0, te_lo = 0, te_hi = 0;
   int64_t ntr = 0, nte = 0, pitch = 0, test_off = 0, ntiles = 0;
-  DevBuf S, pool, elite[2], y_store, part, sse, ticket;
+  DevBuf S, pool, elite[2], y_store, part, sse, sse64, ticket;
 };
 
 void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, int64_t ntr,
@@ -282,6 +282,8 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
     p->y_store.alloc(p->pitch * 8);
     p->part.alloc(m * p->ntiles * 2 * 8);
     p->sse.alloc(m * 2 * 8);
+    p->sse64.alloc(m * 2 * 8);
+    GSGP_CUDA(cudaMemsetAsync(p->sse64.p, 0, m * 2 * 8, st));
     p->ticket.alloc(16);
     GSGP_CUDA(cudaMemsetAsync(p->ticket.p, 0, 16, st));
     GSGP_CUDA(cudaMemsetAsync(p->S.p, 0, m * p->pitch * esz, st));
@@ -331,7 +333,7 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
     ipart.alloc(m * itiles * 2 * 8);
     ia.part = ipart.as<double>();
     launch_interpret(ia, INTERP_POP, st);
-    launch_reduce_partials(ipart.as<double>(), m, itiles, p->sse.as<double>(), false, st);
+    launch_reduce_partials(ipart.as<double>(), m, itiles, p->sse64.as<double>(), false, st);
     // pool: stream base m, same compiled program buffer offset by m genomes
     InterpArgs ip = ia;
     ip.code = ins.as<Ins>() + m * (k + 1);
@@ -342,23 +344,42 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
     ip.wide = nullptr;
     ip.y = nullptr;
     launch_interpret(ip, INTERP_POOL, st);
+    // initial SSE of the stored semantics in the generation kernel's order
+    GsmArgs ga{};
+    ga.pool = p->pool.p;
+    ga.S = p->S.p;
+    ga.elite_prev = p->elite[0].p;
+    ga.elite_cur = p->elite[1].p;
+    ga.y = p->y_store.as<double>();
+    ga.pitch = p->pitch;
+    ga.test_off = p->test_off;
+    ga.m = m;
+    ga.part = p->part.as<double>();
+    ga.ticket = p->ticket.as<unsigned long long>();
+    launch_sse_only(ga, f64, st);
+    launch_reduce_partials(p->part.as<double>(), m, p->ntiles, p->sse.as<double>(), false, st);
     GSGP_CUDA(cudaStreamSynchronize(st));   // temporaries (Xr, XT, ipart) are freed on scope exit
   }
 
   // ---- exchange the initial SSE / overflow flags across shards and ranks
   // G == 1: survival reads shard 0's SSE vector directly (no copy)
+  DevBuf sse64_total;
+  sse64_total.alloc(m * 2 * 8);
   double* sse_vec = G == 1 ? sh[0]->sse.as<double>() : sse_total.as<double>();
-  auto exchange = [&](cudaStream_t s) {
+  double* sse64_vec = G == 1 ? sh[0]->sse64.as<double>() : sse64_total.as<double>();
+  auto exchange_of = [&](DevBuf Shard::*mem, double* dst, cudaStream_t s) {
     if (G > 1) {
       std::vector<const double*> v;
-      for (auto& p : sh) v.push_back(p->sse.as<double>());
-      launch_sum_shards(v.data(), G, m * 2, sse_vec, s);
+      for (auto& p : sh) v.push_back((p.get()->*mem).as<double>());
+      launch_sum_shards(v.data(), G, m * 2, dst, s);
     }
     if (W > 1)
-      nccl().check(nccl().allReduce(sse_vec, sse_vec, m * 2, ncclFloat64, ncclSum, cs.comm, s),
+      nccl().check(nccl().allReduce(dst, dst, m * 2, ncclFloat64, ncclSum, cs.comm, s),
                    "ncclAllReduce(sse)");
   };
+  auto exchange = [&](cudaStream_t s) { exchange_of(&Shard::sse, sse_vec, s); };
   exchange(st);
+  exchange_of(&Shard::sse64, sse64_vec, st);
   if (W > 1) {
     DevBuf bits;
     bits.alloc(m * 2 * 4);
@@ -375,6 +396,7 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   sa.ntr = (double)ntr;
   sa.nte = (double)nte;
   sa.sse_off = sse_vec;
+  sa.sse_alt = sse64_vec;
   sa.F = F.as<double>();
   sa.TS = TS.as<double>();
   sa.wide = wide.as<int32_t>();

@@ -121,7 +121,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // count (mutation.py:86).  In the engine the parent is finite (or an fp32
 // overflow slot whose fp64 value the reference keeps constant)
 // so no replacement is done there.
-template <typename T, bool kOp>
+// kSseOnly: no mutation and no stores — the SSE of the stored semantics in
+// exactly the order a generation uses, for the initial fitness (so an
+// offspring that equals its parent bit for bit ties with it, as in numpy).
+template <typename T, bool kOp, bool kSseOnly = false>
 __global__ void __launch_bounds__(kTmaThreads, 1)
 k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t nunits) {
   using Vec = typename Vec16<T>::type;
@@ -215,9 +218,10 @@ k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t nunits) {
         const int64_t t = unit / m, i = unit - t * m;
         const int64_t off = t * TILE;
         const int64_t n = min((int64_t)TILE, a.pitch - off);
-        int64_t ui, vi;
-        double msd;
-        if (a.plan_inline) {
+        int64_t ui = 0, vi = 0;
+        double msd = 0.0;
+        if (kSseOnly) {
+        } else if (a.plan_inline) {
           plan_slot(plan_key, i, a.plan.r, a.plan.ms_uniform, a.plan.ms_const, &ui, &vi, &msd);
           if (t == 0 && a.write_plan) { u_out[i] = ui; v_out[i] = vi; ms_out[i] = msd; }
         } else {
@@ -230,10 +234,12 @@ k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t nunits) {
         T* d = data + (int64_t)s * 3 * TILE;
         slot_unit[s] = unit;
         slot_ms[s] = msd;
-        mbar_expect_tx(full + s, 3 * bytes);
+        mbar_expect_tx(full + s, (kSseOnly ? 1 : 3) * bytes);
         bulk_g2s(d, src + off, bytes, full + s, stream);
-        bulk_g2s(d + TILE, pool + ui * a.pitch + off, bytes, full + s, keep);
-        bulk_g2s(d + 2 * TILE, pool + vi * a.pitch + off, bytes, full + s, keep);
+        if (!kSseOnly) {
+          bulk_g2s(d + TILE, pool + ui * a.pitch + off, bytes, full + s, keep);
+          bulk_g2s(d + 2 * TILE, pool + vi * a.pitch + off, bytes, full + s, keep);
+        }
         if (++s == kStages) { s = 0; ++j; }
       }
       // every claim of this CTA is done; the last CTA out re-arms the ticket
@@ -309,8 +315,10 @@ k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t nunits) {
     for (int q = 0; q < VPT; ++q) {
       const int e = (q * kNCT + ct) * EV;
       P[q] = *reinterpret_cast<const Vec*>(d + e);
-      A[q] = *reinterpret_cast<const Vec*>(d + TILE + e);
-      B[q] = *reinterpret_cast<const Vec*>(d + 2 * TILE + e);
+      if (!kSseOnly) {
+        A[q] = *reinterpret_cast<const Vec*>(d + TILE + e);
+        B[q] = *reinterpret_cast<const Vec*>(d + 2 * TILE + e);
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty + s);   // stage free: the producer refills while we compute
@@ -330,14 +338,16 @@ k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t nunits) {
       double sacc = 0.0;
 #pragma unroll
       for (int c = 0; c < EV; ++c) {
-        T o = mut(pe[c], ae[c], be[c], msv, a.sign);
+        T o = kSseOnly ? pe[c] : mut(pe[c], ae[c], be[c], msv, a.sign);
         if (kOp && !isfinite((double)o)) { o = (T)0; ++nonfinite; }
         oe[c] = o;
         const double dd = __dsub_rn((double)o, y[q][c]);
         sacc = __fma_rn(dd, dd, sacc);   // one fused op: fewer fp64 issues (power-bound)
       }
-      __stcs(reinterpret_cast<Vec*>(orow + e), O);
-      if (save) __stcs(reinterpret_cast<Vec*>(elite_cur + off + e), P[q]);
+      if (!kSseOnly) {
+        __stcs(reinterpret_cast<Vec*>(orow + e), O);
+        if (save) __stcs(reinterpret_cast<Vec*>(elite_cur + off + e), P[q]);
+      }
       if (off + e < a.test_off) acc_tr = __dadd_rn(acc_tr, sacc);
       else acc_te = __dadd_rn(acc_te, sacc);
     }
@@ -372,6 +382,12 @@ int64_t gsm_tiles(int64_t pitch, bool f64) {
 }
 
 void launch_gsm(const GsmArgs& a, bool f64, bool operator_mode, cudaStream_t s) {
+  launch_gsm_mode(a, f64, operator_mode ? 1 : 0, s);
+}
+
+void launch_sse_only(const GsmArgs& a, bool f64, cudaStream_t s) { launch_gsm_mode(a, f64, 2, s); }
+
+void launch_gsm_mode(const GsmArgs& a, bool f64, int mode, cudaStream_t s) {
   if (a.m <= 0 || a.pitch <= 0) return;
   GSGP_REQUIRE(a.pitch % 32 == 0, "storage pitch must be a multiple of 32");
   const int64_t ntiles = gsm_tiles(a.pitch, f64);
@@ -387,8 +403,15 @@ void launch_gsm(const GsmArgs& a, bool f64, bool operator_mode, cudaStream_t s) 
     GSGP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
     kern<<<grid, kTmaThreads, kTmaSmem, s>>>(a, ntiles, nunits);
   };
-  if (f64) operator_mode ? go(k_gsm_tma<double, true>) : go(k_gsm_tma<double, false>);
-  else operator_mode ? go(k_gsm_tma<float, true>) : go(k_gsm_tma<float, false>);
+  if (f64) {
+    if (mode == 1) go(k_gsm_tma<double, true>);
+    else if (mode == 2) go(k_gsm_tma<double, false, true>);
+    else go(k_gsm_tma<double, false>);
+  } else {
+    if (mode == 1) go(k_gsm_tma<float, true>);
+    else if (mode == 2) go(k_gsm_tma<float, false, true>);
+    else go(k_gsm_tma<float, false>);
+  }
   GSGP_CUDA(cudaGetLastError());
 }
 

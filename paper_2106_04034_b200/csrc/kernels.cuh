@@ -121,6 +121,11 @@ struct GsmArgs {
 };
 int64_t gsm_tiles(int64_t pitch, bool f64);
 void launch_gsm(const GsmArgs& a, bool f64, bool operator_mode, cudaStream_t s);
+// SSE of the stored semantics S against y in the generation kernel's exact
+// order (no mutation, no stores): part[m][ntiles][2]
+void launch_sse_only(const GsmArgs& a, bool f64, cudaStream_t s);
+// mode 0 engine, 1 operator (non-finite -> 0), 2 SSE only
+void launch_gsm_mode(const GsmArgs& a, bool f64, int mode, cudaStream_t s);
 
 // sum [rows][ntiles][2] partials (fixed order) into out[rows][2] (+= when accumulate)
 void launch_reduce_partials(const double* part, int64_t rows, int64_t ntiles, double* out,
@@ -136,6 +141,7 @@ struct SurviveArgs {
   int64_t m;
   double ntr, nte;
   const double* sse_off;    // [m][2] offspring SSE (train, test), already exchanged
+  const double* sse_alt;    // init only: [m][2] fp64-interpreter SSE, used for fp32-overflow slots
   double* F;                // [m] state train fitness (in: parent, out: next)
   double* TS;               // [m] state test SSE
   int32_t* wide;            // [m] slot flags

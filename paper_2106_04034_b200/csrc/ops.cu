@@ -288,14 +288,18 @@ __global__ void __launch_bounds__(256) k_reduce_survive(const double* __restrict
   if (threadIdx.x == 0) *done = 0;
 }
 
-// evolution.py:132-143: initial fitness, elite and trace[0]
+// evolution.py:132-143: initial fitness, elite and trace[0].  The fitness
+// comes from the stored semantics in the generation kernel's SSE order
+// (sse_off), so a later offspring equal to its parent ties with it exactly;
+// fp32-overflow slots use the fp64 interpreter SSE (sse_alt).
 __global__ void __launch_bounds__(1024) k_init_state(SurviveArgs a) {
   __shared__ ArgVal sh[32];
   ArgVal b = kMinInit;
   for (int64_t i = threadIdx.x; i < a.m; i += blockDim.x) {
-    double f = rmse_of(a.sse_off[2 * i], a.ntr);
+    const int32_t fl = a.wide[i];
+    double f = rmse_of((fl & 1) ? a.sse_alt[2 * i] : a.sse_off[2 * i], a.ntr);
     a.F[i] = f;
-    a.TS[i] = a.sse_off[2 * i + 1];
+    a.TS[i] = (fl & 2) ? a.sse_alt[2 * i + 1] : a.sse_off[2 * i + 1];
     b = better_min(b, ArgVal{f, i});
   }
   b = block_arg<true>(b, sh);
@@ -305,7 +309,7 @@ __global__ void __launch_bounds__(1024) k_init_state(SurviveArgs a) {
     a.rec_slot[0] = b.i;
     a.rec_fit[0] = b.v;
     a.trace_tr[0] = b.v;
-    a.trace_te[0] = rmse_of(a.sse_off[2 * b.i + 1], a.nte);
+    a.trace_te[0] = rmse_of(a.TS[b.i], a.nte);
     a.ctl[CTL_GEN] = 1;
     a.ctl[CTL_BP] = b.i;
     a.ctl[CTL_REDIRECT] = -1;

@@ -238,6 +238,20 @@ RUNS = {
             (4000, 8, 1), (1000, 2), "bench"),
     "g0": (dict(population_size=12, random_trees=12, program_size=21, generations=0, seed=5),
            (30, 3, 1), (10, 2), "toy"),
+    # edge cases: single individual, k=1, one fitness case, degenerate gene mixes
+    "m1": (dict(population_size=1, random_trees=2, program_size=7, generations=10, seed=3),
+           (5, 2, 3), (3, 4), "toy"),
+    "k1": (dict(population_size=5, random_trees=3, program_size=1, generations=8, seed=8),
+           (9, 2, 5), (4, 6), "toy"),
+    "n1": (dict(population_size=6, random_trees=4, program_size=15, generations=10, seed=9),
+           (1, 3, 7), (1, 8), "toy"),
+    "const": (dict(population_size=8, random_trees=4, program_size=5, generations=10, seed=10,
+                   p_function=0.0, p_feature=0.0, p_constant=1.0), (12, 2, 9), (5, 10), "toy"),
+    "funcs": (dict(population_size=6, random_trees=3, program_size=9, generations=6, seed=11,
+                   p_function=1.0, p_feature=0.0, p_constant=0.0), (10, 2, 11), (4, 12), "toy"),
+    # 5 initial rows exceed FLT_MAX: exercises the engine's fp32-overflow slots
+    "wide": (dict(population_size=1024, random_trees=64, program_size=1024, generations=40, seed=2),
+             (300, 5, 1), (100, 2), "bench"),
 }
 
 

@@ -20,7 +20,8 @@ from oracle import engine32, restate as R
 RTOL = 1e-5
 
 
-@pytest.mark.parametrize("name", ["tiny", "small", "plus", "g0", "accept", "c1", "c2s"])
+@pytest.mark.parametrize("name", ["tiny", "small", "plus", "g0", "accept", "c1", "c2s", "wide", "m1",
+                                  "k1", "n1", "const", "funcs"])
 def test_fp32_storage_reproduces_reference(name):
     g = golden(f"run_{name}")
     cfg = R.Cfg(**ast.literal_eval(str(g["cfg"][0])))
@@ -36,15 +37,19 @@ def test_fp32_storage_reproduces_reference(name):
     assert out["overflow"] == int(g["overflow"][0])
 
 
-def test_c1_has_fp32_overflow_slots_and_still_matches():
-    """k=1024 genomes overflow fp32 in a few rows (SURVEY §7 hard part 3); the
-    engine keeps those slots' fp64 fitness constant, as the reference's
-    values are (|x| > FLT_MAX absorbs any |delta| <= 2)."""
-    g = golden("run_c1")
+def test_fp32_overflow_slots_are_needed_and_sufficient():
+    """k=1024 genomes overflow fp32 in a few rows (SURVEY §7 hard part 3).  In
+    the reference those values never change (|x| > FLT_MAX absorbs any
+    |delta| <= 2), so the slot's fitness is constant; the engine keeps it.
+    Golden run 'wide' has 5 such rows: with the mechanism the elite trace is
+    the reference's, without it argmax ties among inf rows pick other slots."""
+    g = golden("run_wide")
     cfg = R.Cfg(**ast.literal_eval(str(g["cfg"][0])))
     out = engine32.run32(cfg, g["Xtr"], g["ytr"], g["Xte"], g["yte"])
-    assert np.array_equal(out["train"], out["train"])  # ran
+    assert sorted(np.nonzero(out["wide0"])[0].tolist()) == [181, 394, 513, 585, 921]
     assert [e[2] for e in out["elite"]] == g["slot"].tolist()
+    plain = engine32.run32(cfg, g["Xtr"], g["ytr"], g["Xte"], g["yte"], wide_slots=False)
+    assert [e[2] for e in plain["elite"]] != g["slot"].tolist()
 
 
 def test_gsm_step32_rounding_order():

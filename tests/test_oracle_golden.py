@@ -88,7 +88,8 @@ def test_fitness_plan_gsm_survival_bit_exact():
     assert np.array_equal(X, g["bench_X"]) and np.array_equal(y, g["bench_y"])
 
 
-@pytest.mark.parametrize("name", ["tiny", "small", "plus", "g0", "accept", "c1"])
+@pytest.mark.parametrize("name", ["tiny", "small", "plus", "g0", "accept", "c1", "wide", "m1", "k1",
+                                  "n1", "const", "funcs"])
 def test_full_run_bit_exact(name):
     g = golden(f"run_{name}")
     cfg = R.Cfg(**ast.literal_eval(str(g["cfg"][0])))
