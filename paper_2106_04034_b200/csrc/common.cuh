@@ -84,17 +84,26 @@ struct __align__(16) Ins {
   uint8_t op;    // InsOp
   uint8_t ls;    // InsSrc of the left operand (or the LOAD source)
   uint8_t rs;    // InsSrc of the right operand
-  uint8_t kind;  // dispatch key: op*16 + ls*4 + rs; LOAD: 64 + ls; PUSH: 80
+  uint8_t kind;  // dense dispatch key 0..38, see ins_kind()
   uint16_t lf;   // feature index when ls == SRC_FEAT
   uint16_t rf;   // feature index when rs == SRC_FEAT
   double c;      // constant when ls or rs == SRC_CONST (never both)
 };
 static_assert(sizeof(Ins) == 16, "Ins must be 16 bytes");
-constexpr int kKindLoad = 64, kKindPush = 80;
+// Dense dispatch keys: the 9 possible operand-source pairs of a binary op
+// (index kPair[ls][rs]) x 4 operators = 0..35, LOAD feature 36, LOAD
+// constant 37, PUSH 38.  Dense keys let the interpreter's switch compile to
+// one jump table.
+constexpr int kKindLoadFeat = 36, kKindLoadConst = 37, kKindPush = 38;
+__host__ __device__ __forceinline__ int ins_pair(int ls, int rs) {
+  // rows: ls = ACC, POP, FEAT, CONST; cols: rs = ACC, POP, FEAT, CONST
+  constexpr int8_t kPair[4][4] = {{-1, 0, 2, 3}, {1, -1, -1, -1}, {4, -1, 6, 7}, {5, -1, 8, -1}};
+  return kPair[ls][rs];
+}
 __host__ __device__ __forceinline__ uint8_t ins_kind(const Ins& in) {
   if (in.op == INS_PUSH) return kKindPush;
-  if (in.op == INS_LOAD) return (uint8_t)(kKindLoad + in.ls);
-  return (uint8_t)(in.op * 16 + in.ls * 4 + in.rs);
+  if (in.op == INS_LOAD) return in.ls == SRC_FEAT ? kKindLoadFeat : kKindLoadConst;
+  return (uint8_t)(ins_pair(in.ls, in.rs) * 4 + in.op);
 }
 
 // binary op with the reference's protected division (interpreter.py:58-65):

@@ -17,6 +17,8 @@
 // for ILP) over a block-uniform instruction stream — every branch is
 // warp-uniform — with the block's feature tile and spill stacks in shared
 // memory.
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace gsgp {
@@ -147,9 +149,9 @@ __global__ void k_compile(const uint8_t* __restrict__ tags, const int32_t* __res
 
 // Per-thread evaluation state for CPT cases, with one fully specialised body
 // per instruction kind (operator x left source x right source).
-template <int CPT, bool kXSmem>
+template <int NT, int CPT, bool kXSmem>
 struct Frame {
-  static constexpr int B = 128, TILE = B * CPT;
+  static constexpr int B = NT, TILE = B * CPT;
   double (&acc)[CPT];
   double* stack;               // [depth][TILE] spill stack
   const double* xs;            // [l][TILE] feature tile (kXSmem)
@@ -159,23 +161,34 @@ struct Frame {
   int tid;
   double eps;
 
+  // operand base for this instruction: the per-case offsets c*B are then
+  // immediates of the shared-memory loads (no per-case address arithmetic)
   template <int S>
-  __device__ __forceinline__ double get(int c, int sp, int f, double cst) const {
-    const int cc = c * B + tid;
-    if constexpr (S == SRC_ACC) return acc[c];
-    else if constexpr (S == SRC_POP) return stack[sp * TILE + cc];
+  __device__ __forceinline__ const double* base(int sp, int f) const {
+    if constexpr (S == SRC_POP) return stack + sp * TILE + tid;
     else if constexpr (S == SRC_FEAT) {
-      if constexpr (kXSmem) return xs[f * TILE + cc];
-      else return valid[c] ? XT[f * xt_pitch + q0 + cc] : 0.0;
+      if constexpr (kXSmem) return xs + f * TILE + tid;
+      else return XT + f * xt_pitch + q0 + tid;
+    } else return nullptr;
+  }
+  template <int S>
+  __device__ __forceinline__ double get(int c, const double* b, double cst) const {
+    if constexpr (S == SRC_ACC) return acc[c];
+    else if constexpr (S == SRC_POP) return b[c * B];
+    else if constexpr (S == SRC_FEAT) {
+      if constexpr (kXSmem) return b[c * B];
+      else return valid[c] ? b[c * B] : 0.0;
     } else return cst;
   }
   // the reference's binary op, one IEEE rounding per case (interpreter.py:58-65)
   template <int OP, int LS, int RS>
   __device__ __forceinline__ void op(int& sp, int lf, int rf, double cst) {
     if constexpr (LS == SRC_POP || RS == SRC_POP) --sp;
+    const double* lb = base<LS>(sp, lf);
+    const double* rb = base<RS>(sp, rf);
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
-      const double l = get<LS>(c, sp, lf, cst), r = get<RS>(c, sp, rf, cst);
+      const double l = get<LS>(c, lb, cst), r = get<RS>(c, rb, cst);
       double v;
       if constexpr (OP == OP_ADD) v = __dadd_rn(l, r);
       else if constexpr (OP == OP_SUB) v = __dsub_rn(l, r);
@@ -186,19 +199,21 @@ struct Frame {
   }
   template <int S>
   __device__ __forceinline__ void load(int& sp, int f, double cst) {
+    const double* b = base<S>(sp, f);
 #pragma unroll
-    for (int c = 0; c < CPT; ++c) acc[c] = get<S>(c, sp, f, cst);
+    for (int c = 0; c < CPT; ++c) acc[c] = get<S>(c, b, cst);
   }
   __device__ __forceinline__ void push(int& sp) {
+    double* b = stack + sp * TILE + tid;
 #pragma unroll
-    for (int c = 0; c < CPT; ++c) stack[sp * TILE + c * B + tid] = acc[c];
+    for (int c = 0; c < CPT; ++c) b[c * B] = acc[c];
     ++sp;
   }
 };
 
-template <int CPT, int MODE, typename TOut, bool kXSmem>
-__global__ void __launch_bounds__(128) k_interpret(InterpArgs a, int64_t ntiles, int64_t gpb) {
-  constexpr int B = 128;
+template <int NT, int CPT, int MODE, typename TOut, bool kXSmem>
+__global__ void __launch_bounds__(NT) k_interpret(InterpArgs a, int64_t ntiles, int64_t gpb) {
+  constexpr int B = NT;
   constexpr int TILE = B * CPT;
   extern __shared__ double smem[];
   const int tid = threadIdx.x;
@@ -239,7 +254,7 @@ __global__ void __launch_bounds__(128) k_interpret(InterpArgs a, int64_t ntiles,
 #pragma unroll
     for (int c = 0; c < CPT; ++c) acc[c] = 0.0;
     int sp = 0;
-    Frame<CPT, kXSmem> fr{acc, stack, xs, a.XT, a.xt_pitch, q0, valid, tid, a.eps};
+    Frame<NT, CPT, kXSmem> fr{acc, stack, xs, a.XT, a.xt_pitch, q0, valid, tid, a.eps};
     uint4 nxt = len > 0 ? __ldg(code) : make_uint4(0, 0, 0, 0);
     for (int i = 0; i < len; ++i) {
       const uint4 raw = nxt;
@@ -250,22 +265,23 @@ __global__ void __launch_bounds__(128) k_interpret(InterpArgs a, int64_t ntiles,
       // one warp-uniform indirect branch per instruction; every case body is
       // straight-line code over the CPT cases of this thread
       switch (kind) {
-#define GSGP_K(OP, LS, RS) \
-  case OP * 16 + LS * 4 + RS: fr.template op<OP, LS, RS>(sp, lf, rf, cst); break;
-#define GSGP_K4(LS, RS) GSGP_K(0, LS, RS) GSGP_K(1, LS, RS) GSGP_K(2, LS, RS) GSGP_K(3, LS, RS)
-        GSGP_K4(SRC_ACC, SRC_POP)
-        GSGP_K4(SRC_POP, SRC_ACC)
-        GSGP_K4(SRC_ACC, SRC_FEAT)
-        GSGP_K4(SRC_ACC, SRC_CONST)
-        GSGP_K4(SRC_FEAT, SRC_ACC)
-        GSGP_K4(SRC_CONST, SRC_ACC)
-        GSGP_K4(SRC_FEAT, SRC_FEAT)
-        GSGP_K4(SRC_FEAT, SRC_CONST)
-        GSGP_K4(SRC_CONST, SRC_FEAT)
+#define GSGP_K(PAIR, OP, LS, RS) \
+  case PAIR * 4 + OP: fr.template op<OP, LS, RS>(sp, lf, rf, cst); break;
+#define GSGP_K4(PAIR, LS, RS) \
+  GSGP_K(PAIR, 0, LS, RS) GSGP_K(PAIR, 1, LS, RS) GSGP_K(PAIR, 2, LS, RS) GSGP_K(PAIR, 3, LS, RS)
+        GSGP_K4(0, SRC_ACC, SRC_POP)
+        GSGP_K4(1, SRC_POP, SRC_ACC)
+        GSGP_K4(2, SRC_ACC, SRC_FEAT)
+        GSGP_K4(3, SRC_ACC, SRC_CONST)
+        GSGP_K4(4, SRC_FEAT, SRC_ACC)
+        GSGP_K4(5, SRC_CONST, SRC_ACC)
+        GSGP_K4(6, SRC_FEAT, SRC_FEAT)
+        GSGP_K4(7, SRC_FEAT, SRC_CONST)
+        GSGP_K4(8, SRC_CONST, SRC_FEAT)
 #undef GSGP_K4
 #undef GSGP_K
-        case kKindLoad + SRC_FEAT: fr.template load<SRC_FEAT>(sp, lf, cst); break;
-        case kKindLoad + SRC_CONST: fr.template load<SRC_CONST>(sp, lf, cst); break;
+        case kKindLoadFeat: fr.template load<SRC_FEAT>(sp, lf, cst); break;
+        case kKindLoadConst: fr.template load<SRC_CONST>(sp, lf, cst); break;
         case kKindPush: fr.push(sp); break;
         default: __trap();   // the compiler never emits any other kind
       }
@@ -318,11 +334,22 @@ __global__ void __launch_bounds__(128) k_interpret(InterpArgs a, int64_t ntiles,
   if ((tid & 31) == 0 && nonfinite) atomicAdd(a.nonfinite, nonfinite);
 }
 
-int choose_cpt(int l) { return l <= 16 ? 4 : (l <= 48 ? 2 : 1); }
+// (threads per block, cases per thread): more cases per thread amortise the
+// per-instruction dispatch; the case tile (features + spill stacks) lives in
+// shared memory, so wide feature sets use smaller tiles.
+struct InterpCfg {
+  int nt, cpt;
+};
+constexpr InterpCfg kInterpCfgs[] = {{128, 4}, {128, 2}, {128, 1}, {64, 8}};
+int choose_cfg(int l) {
+  static const int forced = getenv("GSGP_INTERP_CFG") ? atoi(getenv("GSGP_INTERP_CFG")) : -1;
+  if (forced >= 0 && forced < 4) return forced;
+  return l <= 16 ? 0 : (l <= 48 ? 1 : 2);
+}
 
-template <int CPT, int MODE, typename TOut>
+template <int NT, int CPT, int MODE, typename TOut>
 void launch_cpt(const InterpArgs& a, cudaStream_t s) {
-  constexpr int TILE = 128 * CPT;
+  constexpr int TILE = NT * CPT;
   const int64_t N = a.ntr + a.nte;
   const int64_t ntiles = (N + TILE - 1) / TILE;
   const size_t stack_bytes = (size_t)(a.maxdepth > 0 ? a.maxdepth : 1) * TILE * sizeof(double);
@@ -339,23 +366,24 @@ void launch_cpt(const InterpArgs& a, cudaStream_t s) {
   GSGP_REQUIRE(gy <= 65535, "too many genome groups");
   dim3 grid((unsigned)ntiles, (unsigned)gy);
   if (xsmem) {
-    auto k = k_interpret<CPT, MODE, TOut, true>;
+    auto k = k_interpret<NT, CPT, MODE, TOut, true>;
     GSGP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k<<<grid, 128, smem, s>>>(a, ntiles, gpb);
+    k<<<grid, NT, smem, s>>>(a, ntiles, gpb);
   } else {
-    auto k = k_interpret<CPT, MODE, TOut, false>;
+    auto k = k_interpret<NT, CPT, MODE, TOut, false>;
     GSGP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k<<<grid, 128, smem, s>>>(a, ntiles, gpb);
+    k<<<grid, NT, smem, s>>>(a, ntiles, gpb);
   }
   GSGP_CUDA(cudaGetLastError());
 }
 
 template <int MODE, typename TOut>
 void launch_mode(const InterpArgs& a, cudaStream_t s) {
-  switch (choose_cpt(a.l)) {
-    case 4: launch_cpt<4, MODE, TOut>(a, s); break;
-    case 2: launch_cpt<2, MODE, TOut>(a, s); break;
-    default: launch_cpt<1, MODE, TOut>(a, s); break;
+  switch (choose_cfg(a.l)) {
+    case 0: launch_cpt<128, 4, MODE, TOut>(a, s); break;
+    case 1: launch_cpt<128, 2, MODE, TOut>(a, s); break;
+    case 2: launch_cpt<128, 1, MODE, TOut>(a, s); break;
+    default: launch_cpt<64, 8, MODE, TOut>(a, s); break;
   }
 }
 
@@ -370,9 +398,9 @@ void launch_compile(const uint8_t* tags, const int32_t* codes, const double* con
 }
 
 int64_t interp_tiles(const InterpArgs& a, int* cpt_out) {
-  int cpt = choose_cpt(a.l);
-  if (cpt_out) *cpt_out = cpt;
-  int64_t tile = 128 * cpt;
+  const InterpCfg c = kInterpCfgs[choose_cfg(a.l)];
+  if (cpt_out) *cpt_out = c.cpt;
+  const int64_t tile = (int64_t)c.nt * c.cpt;
   return (a.ntr + a.nte + tile - 1) / tile;
 }
 
