@@ -19,6 +19,10 @@ from .ops import (
     create_population, derive_seed, gsm, gsm_paired, gsm_step_f32, interpret, rmse, rng_bits,
     rng_stream, sample_gene, sigmoid, sigmoid_array, uniform_array,
 )
-from .harness import make_benchmark_dataset
+from .harness import make_benchmark_dataset, sweep, timed_run
+from .io_cli import (
+    load_config, load_dataset, read_lineage_sidecar, run_cli, write_dataset,
+    write_lineage_sidecar, write_traces,
+)
 
 __version__ = "0.1.0"

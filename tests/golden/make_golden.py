@@ -285,10 +285,31 @@ def gen_runs():
         print(f"run {name}: {dt:.1f}s, parent elites {int((src == 0).sum())}/{len(src)}")
 
 
+def gen_cli():
+    """The reference CLI's own files for a 2-run job (pkg/src/gsgp/io_cli.py)."""
+    import shutil
+    from gsgp import run_cli, write_dataset
+    d = OUT / "cli_ref"
+    if d.exists():
+        shutil.rmtree(d)
+    d.mkdir()
+    write_dataset(d / "train.txt", make_benchmark_dataset(60, 3, seed=6))
+    write_dataset(d / "test.txt", make_benchmark_dataset(20, 3, seed=7))
+    (d / "config.ini").write_text(
+        "# reference-format config\n[run]\npopulation_size = 24\nrandom_trees = 16\n"
+        "program_size = 31\ngenerations = 12\nruns = 2\nseed = 4242\nmutation_step = uniform\n")
+    out = d / "out"
+    code = run_cli(["-train_file", str(d / "train.txt"), "-test_file", str(d / "test.txt"),
+                    "-config", str(d / "config.ini"), "-output_dir", str(out), "-backend", "sequential"])
+    assert code == 0
+    (out / "timings.csv").unlink()   # wall-clock values: not a fixture
+
+
 if __name__ == "__main__":
     gen_rng()
     gen_population()
     gen_interpreter()
     gen_ops()
     gen_runs()
+    gen_cli()
     print("golden fixtures written to", OUT)
