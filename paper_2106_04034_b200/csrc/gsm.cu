@@ -142,6 +142,7 @@ k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t nunits) {
   int64_t* slot_unit = reinterpret_cast<int64_t*>(rempty + kRedStages);   // [S] unit in stage
   int64_t* red_unit = slot_unit + kStages;                                // [RS] unit in red slot
   double* slot_ms = reinterpret_cast<double*>(red_unit + kRedStages);     // [S] mutation step
+  int2* slot_it = reinterpret_cast<int2*>(slot_ms + kStages);             // [S] (row i, tile t)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t m = a.m;
@@ -197,16 +198,23 @@ k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t nunits) {
       int s = 0;
       uint32_t j = 0;
       // tickets are claimed kBatch units at a time, one claim ahead, so the
-      // atomic's round trip overlaps the current units' copies
+      // atomic's round trip overlaps the current units' copies.  (Claiming
+      // several batches ahead and bulk-prefetching their parent tiles into
+      // L2 was measured slower on every config: profiles/r01/README.md.)
       constexpr int kBatch = 2;
       int64_t next = (int64_t)atomicAdd(a.ticket, (unsigned long long)kBatch);
-      int64_t base = 0;
+      int64_t base = 0, t = 0, i = 0;
       int in_batch = kBatch;
       for (int64_t k = 0;; ++k) {
         if (in_batch == kBatch) {
           base = next;
-          in_batch = 0;
           if (base < nunits) next = (int64_t)atomicAdd(a.ticket, (unsigned long long)kBatch);
+          in_batch = 0;
+          t = base / m;                 // one division per claimed batch
+          i = base - t * m;
+        } else if (++i == m) {          // next unit of the batch: next row (or tile)
+          i = 0;
+          ++t;
         }
         const int64_t unit = base + in_batch++;
         if (k >= kStages) mbar_wait(empty + s, (j & 1) ^ 1);
@@ -215,7 +223,6 @@ k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t nunits) {
           mbar_arrive(full + s);
           break;
         }
-        const int64_t t = unit / m, i = unit - t * m;
         const int64_t off = t * TILE;
         const int64_t n = min((int64_t)TILE, a.pitch - off);
         int64_t ui = 0, vi = 0;
@@ -234,6 +241,7 @@ k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t nunits) {
         T* d = data + (int64_t)s * 3 * TILE;
         slot_unit[s] = unit;
         slot_ms[s] = msd;
+        slot_it[s] = make_int2((int)i, (int)t);
         mbar_expect_tx(full + s, (kSseOnly ? 1 : 3) * bytes);
         bulk_g2s(d, src + off, bytes, full + s, stream);
         if (!kSseOnly) {
@@ -295,7 +303,8 @@ k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t nunits) {
       }
       break;
     }
-    const int64_t t = unit / m, i = unit - t * m;
+    const int2 it = slot_it[s];
+    const int64_t t = it.y, i = it.x;
     const int64_t off = t * TILE;
     const int64_t n = min((int64_t)TILE, a.pitch - off);
     if (t != cur_t) {   // target tile: registers, reloaded when the CTA changes tile
@@ -371,7 +380,7 @@ k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t nunits) {
 }
 
 constexpr size_t kTmaSmem = (size_t)kStages * 3 * kTileBytes + (size_t)kRedStages * kConsumerWarps * 2 * 8 +
-                            (2 * kStages + 2 * kRedStages) * 8 + (2 * kStages + kRedStages) * 8;
+                            (2 * kStages + 2 * kRedStages) * 8 + (3 * kStages + kRedStages) * 8;
 int g_num_sms = 0;
 
 }  // namespace
