@@ -182,13 +182,15 @@ int gsgp_compute_semantics(const uint8_t* tags, const int32_t* codes, const doub
     h2d(dt.p, tags, count * k);
     h2d(dc.p, codes, count * k * 4);
     h2d(dv.p, consts, count * k * 8);
-    Buf ins(count * (k + 1) * sizeof(Ins)), len(count * 4), dep(count * 4), mx(4),
-        scr(count * 4 * k * 4), fl(count * k), cv(count * k * 8);
-    Program prog{ins.as<Ins>(), len.as<int32_t>(), dep.as<int32_t>(), mx.as<int32_t>(),
-                 scr.as<int32_t>(), fl.as<uint8_t>(), cv.as<double>()};
+    Buf ins(count * (k + 1) * sizeof(Ins)), exe(count * (k + 1) * sizeof(Ins)), len(count * 4),
+        nconst(count * 4), ctab(count * k * 8), mx(3 * 4), scr(count * 4 * k * 4), fl(count * k),
+        cv(count * k * 8);
+    Program prog{ins.as<Ins>(), exe.as<Ins>(), len.as<int32_t>(), nconst.as<int32_t>(),
+                 ctab.as<double>(), mx.as<int32_t>(), scr.as<int32_t>(), fl.as<uint8_t>(),
+                 cv.as<double>()};
     launch_compile(dt.as<uint8_t>(), dc.as<int32_t>(), dv.as<double>(), count, (int32_t)k, eps, prog, 0);
-    int32_t maxdepth = 0;
-    d2h(&maxdepth, mx.p, 4);
+    int32_t maxima[3] = {0, 0, 0};
+    d2h(maxima, mx.p, 12);
     Buf xr(n * l * 8), xt(n * l * 8), o(count * n * 8), nf(8);
     h2d(xr.p, X, n * l * 8);
     k_transpose_op<<<nb(n * l), 256>>>(xr.as<double>(), n, l, xt.as<double>());
@@ -196,7 +198,10 @@ int gsgp_compute_semantics(const uint8_t* tags, const int32_t* codes, const doub
     GSGP_CUDA(cudaMemset(nf.p, 0, 8));
     InterpArgs a{};
     a.code = ins.as<Ins>();
+    a.exe = exe.as<Ins>();
     a.len = len.as<int32_t>();
+    a.nconst = nconst.as<int32_t>();
+    a.ctab = ctab.as<double>();
     a.k1 = k + 1;
     a.count = count;
     a.XT = xt.as<double>();
@@ -205,7 +210,9 @@ int gsgp_compute_semantics(const uint8_t* tags, const int32_t* codes, const doub
     a.ntr = n;
     a.nte = 0;
     a.eps = eps;
-    a.maxdepth = maxdepth;
+    a.maxdepth = maxima[0];
+    a.maxconst = maxima[1];
+    a.maxlen = maxima[2];
     a.out64 = o.as<double>();
     a.nonfinite = nf.as<unsigned long long>();
     a.raw = replace_nonfinite ? 0 : 1;

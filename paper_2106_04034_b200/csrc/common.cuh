@@ -75,36 +75,32 @@ enum GeneTag : uint8_t { TAG_FUNCTION = 0, TAG_FEATURE = 1, TAG_CONSTANT = 2 }; 
 enum FunctionOp : int32_t { OP_ADD = 0, OP_SUB = 1, OP_MUL = 2, OP_DIV = 3 };      // core.py:47-51
 
 // One instruction of a compiled (dead-code-eliminated, constant-folded,
-// Sethi-Ullman ordered) genome.  The accumulator machine keeps the running
-// value in a register; spills go to a per-case stack in shared memory.
-enum InsOp : uint8_t { INS_ADD = 0, INS_SUB = 1, INS_MUL = 2, INS_DIV = 3, INS_LOAD = 4, INS_PUSH = 5 };
-enum InsSrc : uint8_t { SRC_ACC = 0, SRC_POP = 1, SRC_FEAT = 2, SRC_CONST = 3 };
+// Sethi-Ullman ordered) genome for the accumulator machine of interp.cu.
+// Every instruction reads one operand x (a feature, a constant-table entry
+// or a static spill-stack slot) and combines it with the accumulator; a
+// node with two leaf children reads a second leaf y instead:
+//   ADD acc+x  SUB acc-x  MUL acc*x  DIV |x|<eps ? 1 : acc/x
+//   RSUB x-acc RDIV |acc|<eps ? 1 : x/acc  LOAD acc=x  PUSHLOAD slot=acc, acc=x
+//   LADD x+y   LSUB x-y   LMUL x*y   LDIV |y|<eps ? 1 : x/y
+// k_compile emits the abstract form (operand class + index); k_link rewrites
+// it for one interpreter configuration into shared-memory byte offsets, so
+// the interpreter fetches x with one address computation and branches once.
+enum InsKind : uint32_t { K_ADD = 0, K_SUB = 1, K_MUL = 2, K_DIV = 3, K_RSUB = 4, K_RDIV = 5,
+                          K_LOAD = 6, K_PUSHLOAD = 7, K_LADD = 8, K_LSUB = 9, K_LMUL = 10,
+                          K_LDIV = 11, K_NUM_KINDS = 12 };
+enum InsClass : uint32_t { X_FEAT = 0, X_CONST = 1, X_STACK = 2 };
 
 struct __align__(16) Ins {
-  uint8_t op;    // InsOp
-  uint8_t ls;    // InsSrc of the left operand (or the LOAD source)
-  uint8_t rs;    // InsSrc of the right operand
-  uint8_t kind;  // dense dispatch key 0..38, see ins_kind()
-  uint16_t lf;   // feature index when ls == SRC_FEAT
-  uint16_t rf;   // feature index when rs == SRC_FEAT
-  double c;      // constant when ls or rs == SRC_CONST (never both)
+  // abstract (compile): a = kind | x class << 8 | y class << 12 | push slot << 16,
+  //                     b = x index, c = y index (L* kinds)
+  // linked (interpret): a = kind | y-is-vector << 8, b = x byte offset,
+  //                     c = y byte offset (L*) or push-slot byte offset (PUSHLOAD),
+  //                     d = x lane mask (~0 vector row, 0 broadcast constant);
+  //                     feature offsets carry kFeatGlobal when features stay in HBM
+  uint32_t a, b, c, d;
 };
 static_assert(sizeof(Ins) == 16, "Ins must be 16 bytes");
-// Dense dispatch keys: the 9 possible operand-source pairs of a binary op
-// (index kPair[ls][rs]) x 4 operators = 0..35, LOAD feature 36, LOAD
-// constant 37, PUSH 38.  Dense keys let the interpreter's switch compile to
-// one jump table.
-constexpr int kKindLoadFeat = 36, kKindLoadConst = 37, kKindPush = 38;
-__host__ __device__ __forceinline__ int ins_pair(int ls, int rs) {
-  // rows: ls = ACC, POP, FEAT, CONST; cols: rs = ACC, POP, FEAT, CONST
-  constexpr int8_t kPair[4][4] = {{-1, 0, 2, 3}, {1, -1, -1, -1}, {4, -1, 6, 7}, {5, -1, 8, -1}};
-  return kPair[ls][rs];
-}
-__host__ __device__ __forceinline__ uint8_t ins_kind(const Ins& in) {
-  if (in.op == INS_PUSH) return kKindPush;
-  if (in.op == INS_LOAD) return in.ls == SRC_FEAT ? kKindLoadFeat : kKindLoadConst;
-  return (uint8_t)(ins_pair(in.ls, in.rs) * 4 + in.op);
-}
+constexpr uint32_t kFeatGlobal = 0x80000000u;
 
 // binary op with the reference's protected division (interpreter.py:58-65):
 // each case rounds exactly once, as numpy does.

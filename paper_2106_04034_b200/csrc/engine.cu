@@ -222,15 +222,17 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   out->shard_train_hi = sh.back()->tr_hi;
 
   // ---- global (replicated) state
-  DevBuf tags, codes, consts, ins, plen, pdepth, pmax, scratch, flags, cval;
+  DevBuf tags, codes, consts, ins, exe, plen, pnconst, ctab, pmax, scratch, flags, cval;
   const int64_t ng = m + r;
   tags.alloc(ng * k);
   codes.alloc(ng * k * 4);
   consts.alloc(ng * k * 8);
   ins.alloc(ng * (k + 1) * sizeof(Ins));
+  exe.alloc(ng * (k + 1) * sizeof(Ins));
   plen.alloc(ng * 4);
-  pdepth.alloc(ng * 4);
-  pmax.alloc(4);
+  pnconst.alloc(ng * 4);
+  ctab.alloc(ng * k * 8);
+  pmax.alloc(3 * 4);
   scratch.alloc(ng * 4 * k * 4);
   flags.alloc(ng * k);
   cval.alloc(ng * k * 8);
@@ -264,12 +266,13 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   GSGP_CUDA(cudaEventRecord(ev_created.e, st));
 
   // ---- compile all m + r genomes once
-  Program prog{ins.as<Ins>(), plen.as<int32_t>(), pdepth.as<int32_t>(), pmax.as<int32_t>(),
-               scratch.as<int32_t>(), flags.as<uint8_t>(), cval.as<double>()};
+  Program prog{ins.as<Ins>(), exe.as<Ins>(), plen.as<int32_t>(), pnconst.as<int32_t>(),
+               ctab.as<double>(), pmax.as<int32_t>(), scratch.as<int32_t>(), flags.as<uint8_t>(),
+               cval.as<double>()};
   launch_compile(tags.as<uint8_t>(), codes.as<int32_t>(), consts.as<double>(), ng, (int32_t)k,
                  cfg->division_eps, prog, st);
-  int32_t maxdepth = 0;
-  GSGP_CUDA(cudaMemcpyAsync(&maxdepth, pmax.p, 4, cudaMemcpyDeviceToHost, st));
+  int32_t maxima[3] = {0, 0, 0};   // {spill depth, constants, instructions}
+  GSGP_CUDA(cudaMemcpyAsync(maxima, pmax.p, 12, cudaMemcpyDeviceToHost, st));
   GSGP_CUDA(cudaStreamSynchronize(st));
 
   // ---- per shard: upload the case slice, interpret population and pool
@@ -311,7 +314,10 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
 
     InterpArgs ia{};
     ia.code = ins.as<Ins>();
+    ia.exe = exe.as<Ins>();
     ia.len = plen.as<int32_t>();
+    ia.nconst = pnconst.as<int32_t>();
+    ia.ctab = ctab.as<double>();
     ia.k1 = k + 1;
     ia.count = m;
     ia.XT = XT.as<double>();
@@ -320,7 +326,9 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
     ia.ntr = p->ntr;
     ia.nte = p->nte;
     ia.eps = cfg->division_eps;
-    ia.maxdepth = maxdepth;
+    ia.maxdepth = maxima[0];
+    ia.maxconst = maxima[1];
+    ia.maxlen = maxima[2];
     ia.out = p->S.p;
     ia.out_is_f64 = f64 ? 1 : 0;
     ia.pitch = p->pitch;
@@ -337,7 +345,10 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
     // pool: stream base m, same compiled program buffer offset by m genomes
     InterpArgs ip = ia;
     ip.code = ins.as<Ins>() + m * (k + 1);
+    ip.exe = exe.as<Ins>() + m * (k + 1);
     ip.len = plen.as<int32_t>() + m;
+    ip.nconst = pnconst.as<int32_t>() + m;
+    ip.ctab = ctab.as<double>() + m * k;
     ip.count = r;
     ip.out = p->pool.p;
     ip.part = nullptr;

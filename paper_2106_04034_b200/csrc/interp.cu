@@ -1,4 +1,5 @@
-// ComputeSemantics on sm_100a: genome compile + case-parallel fp64 interpreter.
+// ComputeSemantics on sm_100a: genome compile + link + case-parallel fp64
+// interpreter.
 //
 // Reference semantics (gsgp/interpreter.py:45-119): postfix scan with a LIFO
 // stack; a function fires only when two operands are stacked (else it is
@@ -11,15 +12,32 @@
 //   * subtrees without a feature are folded to a constant with the same
 //     fp64 operations (bit-identical: each node is a pure IEEE function of
 //     its children);
-//   * children are evaluated in Sethi-Ullman order with terminal operands
-//     folded into the instruction, so the spill stack is <= log2(nodes)+1.
-// The evaluator then runs one thread per fitness case (CPT cases per thread
-// for ILP) over a block-uniform instruction stream — every branch is
-// warp-uniform — with the block's feature tile and spill stacks in shared
-// memory.
+//   * children are evaluated in Sethi-Ullman order on a one-operand
+//     accumulator machine (common.cuh InsKind): every instruction combines
+//     the accumulator with ONE operand x — a feature, a constant-table entry
+//     or a spill slot whose index is static — so the interpreter fetches x
+//     with a single shared-memory address and branches once, on an 8-way
+//     kind.  A node with two leaf children is one L* instruction (x OP y);
+//     a spill (PUSH) is always followed by the LOAD that starts the other
+//     subtree, so the two fuse into PUSHLOAD (then the leaf pair is
+//     PUSHLOAD x + OP y).  ADD/MUL with the accumulator on the
+//     right use commutativity (IEEE + and * are commutative bit for bit);
+//     SUB/DIV use the reversed kinds RSUB/RDIV, so every operand keeps its
+//     role and every node still rounds exactly once.
+// k_link rewrites the abstract operands into byte offsets of the chosen
+// launch configuration (case tile, shared-memory row layout) once per
+// launch.  The evaluator runs one thread per fitness case (CPT cases per
+// thread); each block stages a genome's program and constant table in
+// shared memory and walks it with broadcast loads.
 #include <cstdlib>
 
 #include "kernels.cuh"
+
+namespace gsgp {
+namespace {
+#include "interp_dispatch.inc"
+}  // namespace
+}  // namespace gsgp
 
 namespace gsgp {
 
@@ -28,6 +46,16 @@ namespace {
 constexpr uint8_t F_EXISTS = 0x80, F_CONST = 0x40, F_FEAT = 0x20, F_NEED = 0x1f;
 
 __device__ __forceinline__ bool is_leaf(uint8_t f) { return (f & (F_CONST | F_FEAT)) != 0; }
+
+__device__ __forceinline__ Ins abstract_ins(uint32_t kind, uint32_t cls, uint32_t idx, uint32_t push,
+                                            uint32_t ycls = 0, uint32_t yidx = 0) {
+  Ins in;
+  in.a = kind | (cls << 8) | (ycls << 12) | (push << 16);
+  in.b = idx;
+  in.c = yidx;
+  in.d = 0;
+  return in;
+}
 
 // one thread per genome; scratch is per-genome global memory
 __global__ void k_compile(const uint8_t* __restrict__ tags, const int32_t* __restrict__ codes,
@@ -45,6 +73,7 @@ __global__ void k_compile(const uint8_t* __restrict__ tags, const int32_t* __res
   uint8_t* fl = P.flags + g * (int64_t)k;
   double* cv = P.cval + g * (int64_t)k;
   Ins* out = P.code + g * (int64_t)(k + 1);
+  double* ctab = P.ctab + g * (int64_t)k;
 
   // ---- structural scan (interpreter.py:53-70) with attributes in postfix order
   int32_t sp = 0, last = -1;
@@ -68,7 +97,7 @@ __global__ void k_compile(const uint8_t* __restrict__ tags, const int32_t* __res
         else if (lb) need = na;
         else if (la) need = nb;
         else need = (na == nb) ? na + 1 : (na > nb ? na : nb);
-        fl[j] = F_EXISTS | (uint8_t)need;
+        fl[j] = F_EXISTS | (uint8_t)(need < F_NEED ? need : F_NEED);
       }
     } else if (t == TAG_FEATURE) {
       fl[j] = F_EXISTS | F_FEAT;
@@ -81,210 +110,261 @@ __global__ void k_compile(const uint8_t* __restrict__ tags, const int32_t* __res
   }
   int32_t root = last >= 0 ? last : (sp > 0 ? stk[sp - 1] : -1);
 
-  auto leaf_src = [&](int32_t n, uint8_t& src, uint16_t& f, double& c) {
-    if (fl[n] & F_CONST) { src = SRC_CONST; c = cv[n]; }
-    else { src = SRC_FEAT; f = (uint16_t)C[n]; }
+  int32_t pc = 0, nc = 0, depth = 0;
+  int32_t ssp = 0;            // static spill-stack pointer
+  int32_t pending = -1;       // slot of a PUSH waiting for the next LOAD
+  // operand class / index of the leaf node n (constants go to the table)
+  auto leaf = [&](int32_t n, uint32_t& cls, uint32_t& idx) {
+    if (fl[n] & F_CONST) { cls = X_CONST; idx = (uint32_t)nc; ctab[nc++] = cv[n]; }
+    else { cls = X_FEAT; idx = (uint32_t)C[n]; }
+  };
+  // emit an instruction whose operand is the leaf node n
+  auto emit_leaf = [&](uint32_t kind, int32_t n) {
+    uint32_t cls, idx;
+    leaf(n, cls, idx);
+    uint32_t push = 0;
+    if (pending >= 0) {       // the spill fuses with the LOAD that follows it
+      if (kind != K_LOAD) __trap();
+      kind = K_PUSHLOAD;
+      push = (uint32_t)pending;
+      pending = -1;
+    }
+    out[pc++] = abstract_ins(kind, cls, idx, push);
+  };
+  // acc = acc OP x  (x is the right operand)
+  auto fwd = [](int32_t op) -> uint32_t { return (uint32_t)op; };       // OP_* == K_* for 0..3
+  // acc = x OP acc  (x is the left operand)
+  auto rev = [](int32_t op) -> uint32_t {
+    return op == OP_SUB ? K_RSUB : (op == OP_DIV ? K_RDIV : (uint32_t)op);
   };
 
-  int32_t pc = 0;
-  int depth = 0;
-  if (root < 0 || is_leaf(fl[root])) {
-    Ins in{};
-    in.op = INS_LOAD;
-    if (root < 0) { in.ls = SRC_CONST; in.c = 0.0; }
-    else leaf_src(root, in.ls, in.lf, in.c);
-    in.kind = ins_kind(in);
-    out[pc++] = in;
+  if (root < 0) {
+    out[pc++] = abstract_ins(K_LOAD, X_CONST, 0, 0);
+    ctab[nc++] = 0.0;
+  } else if (is_leaf(fl[root])) {
+    emit_leaf(K_LOAD, root);
   } else {
-    depth = fl[root] & F_NEED;
     // ---- iterative Sethi-Ullman emission; frame = node*4 + state
     int32_t top = 0;
     work[top++] = root * 4;
     while (top > 0) {
-      int32_t fr = work[top - 1];
-      int32_t n = fr >> 2, st = fr & 3;
-      int32_t l = Lc[n], r = Rc[n];
-      bool la = is_leaf(fl[l]), lb = is_leaf(fl[r]);
-      bool both = !la && !lb;
-      bool left_first = both ? ((fl[l] & F_NEED) >= (fl[r] & F_NEED)) : !la;
-      int32_t first = left_first ? l : r, second = left_first ? r : l;
-      if (st == 0 && !(la && lb)) {
-        work[top - 1] = n * 4 + 1;
-        work[top++] = first * 4;
-        continue;
+      const int32_t fr = work[top - 1];
+      const int32_t n = fr >> 2, st = fr & 3;
+      const int32_t l = Lc[n], r = Rc[n];
+      const bool la = is_leaf(fl[l]), lb = is_leaf(fl[r]);
+      const bool left_first = (!la && !lb) ? ((fl[l] & F_NEED) >= (fl[r] & F_NEED)) : !la;
+      const int32_t op = C[n];
+      if (st == 0) {
+        if (la && lb) {
+          if (pending >= 0) {                 // PUSHLOAD l ; acc = acc OP r
+            emit_leaf(K_LOAD, l);
+            emit_leaf(fwd(op), r);
+          } else {                            // acc = l OP r
+            uint32_t xc, xi, yc, yi;
+            leaf(l, xc, xi);
+            leaf(r, yc, yi);
+            out[pc++] = abstract_ins(K_LADD + (uint32_t)op, xc, xi, 0, yc, yi);
+          }
+          --top;
+        } else {
+          work[top - 1] = n * 4 + 1;
+          work[top++] = (left_first ? l : r) * 4;
+        }
+      } else if (st == 1) {
+        if (lb) { emit_leaf(fwd(op), r); --top; }          // acc = L OP r
+        else if (la) { emit_leaf(rev(op), l); --top; }     // acc = l OP R
+        else {                                             // spill, evaluate the other child
+          pending = ssp++;
+          if (ssp > depth) depth = ssp;
+          work[top - 1] = n * 4 + 2;
+          work[top++] = (left_first ? r : l) * 4;
+        }
+      } else {                                             // both children non-leaf
+        const uint32_t slot = (uint32_t)(--ssp);
+        // left evaluated first: stack = L, acc = R -> x OP acc; else stack = R, acc = L
+        out[pc++] = abstract_ins(left_first ? rev(op) : fwd(op), X_STACK, slot, 0);
+        --top;
       }
-      if (st == 1 && both) {
-        Ins p{};
-        p.op = INS_PUSH;
-        p.kind = ins_kind(p);
-        out[pc++] = p;
-        work[top - 1] = n * 4 + 2;
-        work[top++] = second * 4;
-        continue;
-      }
-      Ins in{};
-      in.op = (uint8_t)C[n];
-      if (la && lb) {
-        leaf_src(l, in.ls, in.lf, in.c);
-        leaf_src(r, in.rs, in.rf, in.c);
-      } else if (both) {
-        in.ls = left_first ? SRC_POP : SRC_ACC;
-        in.rs = left_first ? SRC_ACC : SRC_POP;
-      } else if (lb) {                 // right operand is a terminal
-        in.ls = SRC_ACC;
-        leaf_src(r, in.rs, in.rf, in.c);
-      } else {                         // left operand is a terminal
-        leaf_src(l, in.ls, in.lf, in.c);
-        in.rs = SRC_ACC;
-      }
-      in.kind = ins_kind(in);
-      out[pc++] = in;
-      --top;
     }
   }
   P.len[g] = pc;
-  P.depth[g] = depth;
-  atomicMax(P.maxdepth, depth);
+  P.nconst[g] = nc;
+  atomicMax(P.maxima, depth);
+  atomicMax(P.maxima + 1, nc);
+  atomicMax(P.maxima + 2, pc);
 }
 
-// Per-thread evaluation state for CPT cases, with one fully specialised body
-// per instruction kind (operator x left source x right source).
-template <int NT, int CPT, bool kXSmem>
-struct Frame {
-  static constexpr int B = NT, TILE = B * CPT;
-  double (&acc)[CPT];
-  double* stack;               // [depth][TILE] spill stack
-  const double* xs;            // [l][TILE] feature tile (kXSmem)
-  const double* XT;            // [l][xt_pitch] features in global memory (!kXSmem)
-  int64_t xt_pitch, q0;
-  const bool (&valid)[CPT];
-  int tid;
-  double eps;
-
-  // operand base for this instruction: the per-case offsets c*B are then
-  // immediates of the shared-memory loads (no per-case address arithmetic)
-  template <int S>
-  __device__ __forceinline__ const double* base(int sp, int f) const {
-    if constexpr (S == SRC_POP) return stack + sp * TILE + tid;
-    else if constexpr (S == SRC_FEAT) {
-      if constexpr (kXSmem) return xs + f * TILE + tid;
-      else return XT + f * xt_pitch + q0 + tid;
-    } else return nullptr;
-  }
-  template <int S>
-  __device__ __forceinline__ double get(int c, const double* b, double cst) const {
-    if constexpr (S == SRC_ACC) return acc[c];
-    else if constexpr (S == SRC_POP) return b[c * B];
-    else if constexpr (S == SRC_FEAT) {
-      if constexpr (kXSmem) return b[c * B];
-      else return valid[c] ? b[c * B] : 0.0;
-    } else return cst;
-  }
-  // the reference's binary op, one IEEE rounding per case (interpreter.py:58-65)
-  template <int OP, int LS, int RS>
-  __device__ __forceinline__ void op(int& sp, int lf, int rf, double cst) {
-    if constexpr (LS == SRC_POP || RS == SRC_POP) --sp;
-    const double* lb = base<LS>(sp, lf);
-    const double* rb = base<RS>(sp, rf);
-#pragma unroll
-    for (int c = 0; c < CPT; ++c) {
-      const double l = get<LS>(c, lb, cst), r = get<RS>(c, rb, cst);
-      double v;
-      if constexpr (OP == OP_ADD) v = __dadd_rn(l, r);
-      else if constexpr (OP == OP_SUB) v = __dsub_rn(l, r);
-      else if constexpr (OP == OP_MUL) v = __dmul_rn(l, r);
-      else v = fabs(r) < eps ? 1.0 : __ddiv_rn(l, r);
-      acc[c] = v;
-    }
-  }
-  template <int S>
-  __device__ __forceinline__ void load(int& sp, int f, double cst) {
-    const double* b = base<S>(sp, f);
-#pragma unroll
-    for (int c = 0; c < CPT; ++c) acc[c] = get<S>(c, b, cst);
-  }
-  __device__ __forceinline__ void push(int& sp) {
-    double* b = stack + sp * TILE + tid;
-#pragma unroll
-    for (int c = 0; c < CPT; ++c) b[c * B] = acc[c];
-    ++sp;
-  }
+// ---------------------------------------------------------------- configurations
+// (threads per block, cases per thread, features in shared memory?)  More
+// cases per thread amortise the per-instruction dispatch; shared memory
+// holds [features][spill slots][constant rows] of the block's case tile.
+struct InterpCfg {
+  int nt, cpt;
+  bool xsmem;
 };
+constexpr InterpCfg kCfgs[] = {{128, 4, true}, {64, 8, true}, {128, 4, false},
+                               {128, 2, true}, {128, 1, false}, {64, 8, false}};
+constexpr int kNumCfgs = sizeof(kCfgs) / sizeof(kCfgs[0]);
+constexpr size_t kSmemCap = 200 * 1024;
+
+// rows of the case tile + the staged program (16 B per instruction)
+size_t cfg_rows_bytes(const InterpCfg& c, const InterpArgs& a) {
+  const size_t rowb = (size_t)c.nt * c.cpt * 8;
+  const size_t crows = ((size_t)(a.maxconst > 0 ? a.maxconst : 1) + c.nt - 1) / c.nt;
+  return ((c.xsmem ? (size_t)a.l : 0) + (size_t)a.maxdepth + crows) * rowb;
+}
+size_t cfg_smem(const InterpCfg& c, const InterpArgs& a) {
+  // + 1 instruction: the loop prefetches one past the end of the program
+  return cfg_rows_bytes(c, a) + (size_t)((a.maxlen > 0 ? a.maxlen : 1) + 1) * sizeof(Ins);
+}
+
+int choose_cfg(const InterpArgs& a) {
+  static const int forced = getenv("GSGP_INTERP_CFG") ? atoi(getenv("GSGP_INTERP_CFG")) : -1;
+  if (forced >= 0 && forced < kNumCfgs && cfg_smem(kCfgs[forced], a) <= kSmemCap) return forced;
+  // features in shared memory while the tile keeps >= 3 blocks per SM
+  if (cfg_smem(kCfgs[0], a) <= 72 * 1024) return 0;
+  if (cfg_smem(kCfgs[2], a) <= 72 * 1024) return 2;
+  return 4;   // 1 KB rows: always fits (depth <= 31, constants <= k)
+}
+
+// ---------------------------------------------------------------- link
+// abstract operand -> byte offset in the block's shared-memory row layout:
+// rows [0, l) features (xsmem), then maxdepth spill slots, then constant rows
+// (constant j: row j / nt, lane j % nt, replicated for the CPT cases)
+__global__ void k_link(const Ins* __restrict__ code, Ins* __restrict__ exe, const int32_t* __restrict__ len,
+                       int64_t count, int64_t k1, int32_t nt, uint32_t rowb, uint32_t frows,
+                       uint32_t maxdepth) {
+  const int64_t g = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;   // one warp per genome
+  if (g >= count) return;
+  const int32_t n = len[g];
+  // byte offset of an operand; vec = 1 for a per-case row, 0 for a constant
+  auto off = [&](uint32_t cls, uint32_t idx, uint32_t& vec) -> uint32_t {
+    vec = 1;
+    if (cls == X_FEAT) return frows ? idx * rowb : (kFeatGlobal | idx);
+    if (cls == X_STACK) return (frows + idx) * rowb;
+    vec = 0;
+    return (frows + maxdepth + idx / (uint32_t)nt) * rowb + (idx % (uint32_t)nt) * 8u;
+  };
+  for (int32_t i = threadIdx.x % 32; i < n; i += 32) {
+    const Ins in = code[g * k1 + i];
+    const uint32_t kind = in.a & 0xff, xcls = (in.a >> 8) & 0xf, ycls = (in.a >> 12) & 0xf;
+    const uint32_t push = in.a >> 16;
+    uint32_t xvec, yvec = 0;
+    Ins o;
+    o.b = off(xcls, in.b, xvec);
+    o.d = xvec ? 0xffffffffu : 0u;
+    if (kind >= K_LADD) o.c = off(ycls, in.c, yvec);
+    else o.c = (frows + push) * rowb;
+    o.a = kind | (yvec << 8);
+    exe[g * k1 + i] = o;
+  }
+}
+
+// ---------------------------------------------------------------- interpret
+// shared-memory accesses at a 32-bit address (the per-case stride becomes the
+// instruction's immediate offset), so the base is computed once per instruction
+__device__ __forceinline__ double lds_f64(uint32_t p) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(p));
+  return v;
+}
+__device__ __forceinline__ uint4 lds_u128(uint32_t p) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(p));
+  return v;
+}
+
 
 template <int NT, int CPT, int MODE, typename TOut, bool kXSmem>
-__global__ void __launch_bounds__(NT) k_interpret(InterpArgs a, int64_t ntiles, int64_t gpb) {
-  constexpr int B = NT;
-  constexpr int TILE = B * CPT;
-  extern __shared__ double smem[];
+__global__ void __launch_bounds__(NT) k_interpret(InterpArgs a, int64_t ntiles, int64_t gpb,
+                                                  uint32_t crow_off, uint32_t prog_off) {
+  constexpr int TILE = NT * CPT;
+  constexpr uint32_t CSTRIDE = NT * 8;          // bytes between a thread's cases
+  extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x;
+  const uint32_t tid8 = (uint32_t)tid * 8u;
   const int64_t tile = blockIdx.x;
   const int64_t q0 = tile * TILE;
   const int64_t N = a.ntr + a.nte;
-  double* xs = smem;                                  // [l][TILE] when kXSmem
-  double* stack = smem + (kXSmem ? (int64_t)a.l * TILE : 0);   // [maxdepth][TILE]
   __shared__ double red[32];
 
   if (kXSmem) {
-    for (int64_t e = tid; e < (int64_t)a.l * TILE; e += B) {
-      int64_t f = e / TILE, c = e - f * TILE;
-      int64_t q = q0 + c;
+    double* xs = reinterpret_cast<double*>(smem);
+    for (int64_t e = tid; e < (int64_t)a.l * TILE; e += NT) {
+      const int64_t f = e / TILE, c = e - f * TILE;
+      const int64_t q = q0 + c;
       xs[e] = q < N ? a.XT[f * a.xt_pitch + q] : 0.0;
     }
-    __syncthreads();
   }
   double ytr[CPT];
   int64_t col[CPT];
   bool valid[CPT], train[CPT];
 #pragma unroll
   for (int c = 0; c < CPT; ++c) {
-    int64_t q = q0 + c * B + tid;
+    const int64_t q = q0 + c * NT + tid;
     valid[c] = q < N;
     train[c] = q < a.ntr;
     col[c] = train[c] ? q : a.test_off + (q - a.ntr);
     ytr[c] = (MODE == INTERP_POP && valid[c]) ? a.y[q] : 0.0;
   }
+  const double* xg = a.XT + q0 + tid;          // global feature rows (!kXSmem)
+  uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("" : "+r"(sbase));              // keep it in a register (no per-iteration remat)
+  const uint32_t pbase = sbase + prog_off;
+  const int64_t cstride = a.k1 - 1;
   unsigned long long nonfinite = 0;
+
+  // operand fetch: a shared-memory row / broadcast constant, or (features
+  // left in HBM) a coalesced global row
+  auto fetch = [&](uint32_t off, uint32_t mask, double (&v)[CPT]) {
+    if (!kXSmem && (off & kFeatGlobal)) {
+      const double* p = xg + (int64_t)(off & ~kFeatGlobal) * a.xt_pitch;
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) v[c] = valid[c] ? __ldg(p + c * NT) : 0.0;
+    } else {
+      const uint32_t p = sbase + off + (tid8 & mask);
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) v[c] = lds_f64(p + c * CSTRIDE);
+    }
+  };
 
   const int64_t g0 = blockIdx.y * gpb;
   const int64_t g1 = min(a.count, g0 + gpb);
   for (int64_t g = g0; g < g1; ++g) {
-    const uint4* code = reinterpret_cast<const uint4*>(a.code + g * a.k1);
+    // ---- stage genome g: program + constant table (replicated for the CPT
+    // cases of a thread) into shared memory
     const int len = a.len[g];
+    __syncthreads();                            // previous genome done with both
+    {
+      const uint4* src = reinterpret_cast<const uint4*>(a.exe + g * a.k1);
+      uint4* dst = reinterpret_cast<uint4*>(smem + prog_off);
+      for (int i = tid; i < len; i += NT) dst[i] = __ldg(src + i);
+      const int nc = a.nconst[g];
+      const double* ct = a.ctab + g * cstride;
+      for (int e = tid; e < nc * CPT; e += NT) {
+        const int j = e / CPT, c = e - j * CPT;
+        *reinterpret_cast<double*>(smem + crow_off + (uint32_t)(j / NT) * (TILE * 8) +
+                                   (uint32_t)(j % NT) * 8u + (uint32_t)c * CSTRIDE) = ct[j];
+      }
+    }
+    __syncthreads();
+
     double acc[CPT];
 #pragma unroll
     for (int c = 0; c < CPT; ++c) acc[c] = 0.0;
-    int sp = 0;
-    Frame<NT, CPT, kXSmem> fr{acc, stack, xs, a.XT, a.xt_pitch, q0, valid, tid, a.eps};
-    uint4 nxt = len > 0 ? __ldg(code) : make_uint4(0, 0, 0, 0);
+    uint4 nxt = lds_u128(pbase);
     for (int i = 0; i < len; ++i) {
-      const uint4 raw = nxt;
-      if (i + 1 < len) nxt = __ldg(code + i + 1);   // prefetch the next instruction
-      const int kind = raw.x >> 24;
-      const int lf = raw.y & 0xffff, rf = raw.y >> 16;
-      const double cst = __hiloint2double((int)raw.w, (int)raw.z);
-      // one warp-uniform indirect branch per instruction; every case body is
-      // straight-line code over the CPT cases of this thread
-      switch (kind) {
-#define GSGP_K(PAIR, OP, LS, RS) \
-  case PAIR * 4 + OP: fr.template op<OP, LS, RS>(sp, lf, rf, cst); break;
-#define GSGP_K4(PAIR, LS, RS) \
-  GSGP_K(PAIR, 0, LS, RS) GSGP_K(PAIR, 1, LS, RS) GSGP_K(PAIR, 2, LS, RS) GSGP_K(PAIR, 3, LS, RS)
-        GSGP_K4(0, SRC_ACC, SRC_POP)
-        GSGP_K4(1, SRC_POP, SRC_ACC)
-        GSGP_K4(2, SRC_ACC, SRC_FEAT)
-        GSGP_K4(3, SRC_ACC, SRC_CONST)
-        GSGP_K4(4, SRC_FEAT, SRC_ACC)
-        GSGP_K4(5, SRC_CONST, SRC_ACC)
-        GSGP_K4(6, SRC_FEAT, SRC_FEAT)
-        GSGP_K4(7, SRC_FEAT, SRC_CONST)
-        GSGP_K4(8, SRC_CONST, SRC_FEAT)
-#undef GSGP_K4
-#undef GSGP_K
-        case kKindLoadFeat: fr.template load<SRC_FEAT>(sp, lf, cst); break;
-        case kKindLoadConst: fr.template load<SRC_CONST>(sp, lf, cst); break;
-        case kKindPush: fr.push(sp); break;
-        default: __trap();   // the compiler never emits any other kind
-      }
+      const uint4 in = nxt;
+      nxt = lds_u128(pbase + (uint32_t)(i + 1) * 16u);   // next instruction (smem holds len + 1)
+      double x[CPT];
+      fetch(in.y, in.w, x);
+      const uint32_t kind = in.x & 0xff;
+      double y[CPT];
+      if (kind >= K_LADD) fetch(in.z, (in.x & 0x100) ? 0xffffffffu : 0u, y);   // second leaf
+      // one warp-uniform jump (interp_dispatch.inc); each arm is straight-line
+      // code over the CPT cases of this thread, one IEEE rounding per case
+      Dispatch<CPT, CSTRIDE>::run(acc, x, y, kind, sbase + in.z + tid8, a.eps);
     }
     // ---- epilogue: non-finite -> 0.0 counted (core.py:348-356), then store
     double sse_tr = 0.0, sse_te = 0.0;
@@ -294,7 +374,7 @@ __global__ void __launch_bounds__(NT) k_interpret(InterpArgs a, int64_t ntiles, 
       if (!valid[c]) continue;
       double v = acc[c];
       if (!isfinite(v) && !(MODE == INTERP_F64 && a.raw)) { v = 0.0; ++nonfinite; }
-      const int64_t q = q0 + c * B + tid;
+      const int64_t q = q0 + c * NT + tid;
       if (MODE == INTERP_F64) {
         a.out64[g * N + q] = v;
       } else if (MODE == INTERP_POP) {
@@ -323,10 +403,9 @@ __global__ void __launch_bounds__(NT) k_interpret(InterpArgs a, int64_t ntiles, 
       __syncthreads();
       if (tid < 2) {
         double t = 0.0;
-        for (int w = 0; w < B / 32; ++w) t = __dadd_rn(t, red[w * 2 + tid]);
+        for (int w = 0; w < NT / 32; ++w) t = __dadd_rn(t, red[w * 2 + tid]);
         a.part[(g * ntiles + tile) * 2 + tid] = t;
       }
-      __syncthreads();
     }
   }
   // block total of replaced elements (integer: order-independent)
@@ -334,56 +413,44 @@ __global__ void __launch_bounds__(NT) k_interpret(InterpArgs a, int64_t ntiles, 
   if ((tid & 31) == 0 && nonfinite) atomicAdd(a.nonfinite, nonfinite);
 }
 
-// (threads per block, cases per thread): more cases per thread amortise the
-// per-instruction dispatch; the case tile (features + spill stacks) lives in
-// shared memory, so wide feature sets use smaller tiles.
-struct InterpCfg {
-  int nt, cpt;
-};
-constexpr InterpCfg kInterpCfgs[] = {{128, 4}, {128, 2}, {128, 1}, {64, 8}};
-int choose_cfg(int l) {
-  static const int forced = getenv("GSGP_INTERP_CFG") ? atoi(getenv("GSGP_INTERP_CFG")) : -1;
-  if (forced >= 0 && forced < 4) return forced;
-  return l <= 16 ? 0 : (l <= 48 ? 1 : 2);
-}
-
-template <int NT, int CPT, int MODE, typename TOut>
-void launch_cpt(const InterpArgs& a, cudaStream_t s) {
+template <int NT, int CPT, int MODE, typename TOut, bool kXSmem>
+void launch_cfg(const InterpArgs& a, cudaStream_t s) {
   constexpr int TILE = NT * CPT;
+  constexpr InterpCfg c{NT, CPT, kXSmem};
   const int64_t N = a.ntr + a.nte;
   const int64_t ntiles = (N + TILE - 1) / TILE;
-  const size_t stack_bytes = (size_t)(a.maxdepth > 0 ? a.maxdepth : 1) * TILE * sizeof(double);
-  const size_t x_bytes = (size_t)a.l * TILE * sizeof(double);
-  const bool xsmem = x_bytes + stack_bytes <= 160 * 1024;
-  const size_t smem = (xsmem ? x_bytes : 0) + stack_bytes;
-  GSGP_REQUIRE(smem <= 200 * 1024, "interpreter spill stack too deep for shared memory");
+  const uint32_t rowb = TILE * 8;
+  const uint32_t frows = kXSmem ? (uint32_t)a.l : 0u;
+  const size_t smem = cfg_smem(c, a);
+  GSGP_REQUIRE(smem <= kSmemCap, "interpreter tile does not fit in shared memory");
+  // link the programs for this row layout
+  k_link<<<(unsigned)((a.count + 3) / 4), 128, 0, s>>>(a.code, a.exe, a.len, a.count, a.k1, NT, rowb,
+                                                      frows, (uint32_t)a.maxdepth);
+  GSGP_CUDA(cudaGetLastError());
   // genomes per block: enough blocks to fill 148 SMs several times over
-  int64_t want = 148 * 8;
+  const int64_t want = 148 * 8;
   int64_t gpb = (a.count * ntiles + want - 1) / want;
   if (gpb < 1) gpb = 1;
   if (gpb > 64) gpb = 64;
-  int64_t gy = (a.count + gpb - 1) / gpb;
+  const int64_t gy = (a.count + gpb - 1) / gpb;
   GSGP_REQUIRE(gy <= 65535, "too many genome groups");
   dim3 grid((unsigned)ntiles, (unsigned)gy);
-  if (xsmem) {
-    auto k = k_interpret<NT, CPT, MODE, TOut, true>;
-    GSGP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k<<<grid, NT, smem, s>>>(a, ntiles, gpb);
-  } else {
-    auto k = k_interpret<NT, CPT, MODE, TOut, false>;
-    GSGP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k<<<grid, NT, smem, s>>>(a, ntiles, gpb);
-  }
+  auto k = k_interpret<NT, CPT, MODE, TOut, kXSmem>;
+  GSGP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k<<<grid, NT, smem, s>>>(a, ntiles, gpb, (frows + (uint32_t)a.maxdepth) * rowb,
+                           (uint32_t)cfg_rows_bytes(c, a));
   GSGP_CUDA(cudaGetLastError());
 }
 
 template <int MODE, typename TOut>
 void launch_mode(const InterpArgs& a, cudaStream_t s) {
-  switch (choose_cfg(a.l)) {
-    case 0: launch_cpt<128, 4, MODE, TOut>(a, s); break;
-    case 1: launch_cpt<128, 2, MODE, TOut>(a, s); break;
-    case 2: launch_cpt<128, 1, MODE, TOut>(a, s); break;
-    default: launch_cpt<64, 8, MODE, TOut>(a, s); break;
+  switch (choose_cfg(a)) {
+    case 0: launch_cfg<128, 4, MODE, TOut, true>(a, s); break;
+    case 1: launch_cfg<64, 8, MODE, TOut, true>(a, s); break;
+    case 2: launch_cfg<128, 4, MODE, TOut, false>(a, s); break;
+    case 3: launch_cfg<128, 2, MODE, TOut, true>(a, s); break;
+    case 4: launch_cfg<128, 1, MODE, TOut, false>(a, s); break;
+    default: launch_cfg<64, 8, MODE, TOut, false>(a, s); break;
   }
 }
 
@@ -392,13 +459,13 @@ void launch_mode(const InterpArgs& a, cudaStream_t s) {
 void launch_compile(const uint8_t* tags, const int32_t* codes, const double* consts, int64_t count,
                     int32_t k, double eps, Program prog, cudaStream_t s) {
   if (count <= 0) return;
-  GSGP_CUDA(cudaMemsetAsync(prog.maxdepth, 0, sizeof(int32_t), s));
+  GSGP_CUDA(cudaMemsetAsync(prog.maxima, 0, 2 * sizeof(int32_t), s));
   k_compile<<<(unsigned)((count + 63) / 64), 64, 0, s>>>(tags, codes, consts, count, k, eps, prog);
   GSGP_CUDA(cudaGetLastError());
 }
 
 int64_t interp_tiles(const InterpArgs& a, int* cpt_out) {
-  const InterpCfg c = kInterpCfgs[choose_cfg(a.l)];
+  const InterpCfg c = kCfgs[choose_cfg(a)];
   if (cpt_out) *cpt_out = c.cpt;
   const int64_t tile = (int64_t)c.nt * c.cpt;
   return (a.ntr + a.nte + tile - 1) / tile;
@@ -406,6 +473,7 @@ int64_t interp_tiles(const InterpArgs& a, int* cpt_out) {
 
 void launch_interpret(const InterpArgs& a, int mode, cudaStream_t s) {
   if (a.count <= 0 || a.ntr + a.nte <= 0) return;
+  GSGP_REQUIRE(a.maxdepth <= 31, "spill stack deeper than the compiler's labels");
   if (mode == INTERP_F64) launch_mode<INTERP_F64, double>(a, s);
   else if (mode == INTERP_POP) {
     if (a.out_is_f64) launch_mode<INTERP_POP, double>(a, s);

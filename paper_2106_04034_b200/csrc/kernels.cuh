@@ -54,30 +54,36 @@ void launch_plan(const PlanParams& p, int64_t gen, const int64_t* gen_ptr, int64
 
 // ------------------------------------------------------------ compile + interpret
 struct Program {
-  Ins* code;            // [count][k+1]
-  int32_t* len;         // [count]
-  int32_t* depth;       // [count] spill-stack depth
-  int32_t* maxdepth;    // [1] max over genomes (atomicMax)
+  Ins* code;            // [count][k+1] abstract instructions (k_compile)
+  Ins* exe;             // [count][k+1] linked for the launch configuration (k_link)
+  int32_t* len;         // [count] instructions
+  int32_t* nconst;      // [count] constant-table entries
+  double* ctab;         // [count][k] constants referenced by the program
+  int32_t* maxima;      // [3] {spill depth, constants, instructions}: max over genomes
   int32_t* scratch;     // [count][4*k] ints
   uint8_t* flags;       // [count][k]
   double* cval;         // [count][k]
 };
+// maxima[] must be zero before the launch (launch_compile clears it)
 void launch_compile(const uint8_t* tags, const int32_t* codes, const double* consts, int64_t count,
                     int32_t k, double eps, Program prog, cudaStream_t s);
 
 enum InterpMode : int { INTERP_F64 = 0, INTERP_POP = 1, INTERP_POOL = 2 };
 
 struct InterpArgs {
-  const Ins* code;
+  const Ins* code;          // abstract program (count genomes, stride k1)
+  Ins* exe;                 // linked copy, rewritten by every launch_interpret
   const int32_t* len;
+  const int32_t* nconst;
+  const double* ctab;       // [count][k1 - 1]
   int64_t k1;               // instruction stride per genome (k + 1)
   int64_t count;            // genomes
+  int32_t maxdepth, maxconst, maxlen;   // Program::maxima, read back once after compile
   const double* XT;         // [l][ncase_pitch] fp64, feature-major, cases stacked train|test
   int64_t xt_pitch;
   int32_t l;
   int64_t ntr, nte;         // local case counts (stacked index q < ntr is train)
   double eps;
-  int32_t maxdepth;
   // outputs
   double* out64;            // INTERP_F64: [count][ntr+nte]
   void* out;                // INTERP_POP/POOL: [count][pitch] float or double

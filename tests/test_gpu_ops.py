@@ -153,6 +153,68 @@ def test_interpreter_feature_range_and_case_permutation():
     assert np.array_equal(b, a[:, perm])
 
 
+def _wide_exponent_values(rng, n):
+    """fp64 values with exponents spread over the whole range (subnormals,
+    the interpreter's fast-division thresholds 2^-500 / 2^501, huge), signed
+    zeros and values near the protection threshold eps."""
+    v = rng.uniform(1, 2, n) * np.exp2(rng.integers(-1074, 1024, n).astype(np.float64))
+    v[rng.random(n) < 0.5] *= -1
+    special = np.array([0.0, -0.0, 5e-324, -1e-310, 2.0 ** -500, np.nextafter(2.0 ** -500, 0),
+                        2.0 ** 501, np.nextafter(2.0 ** 501, 0), 1e308, -1e308, 1e-6,
+                        np.nextafter(1e-6, 0), -1e-6, 1.0, -3.7])
+    v[: special.size] = special
+    with np.errstate(all="ignore"):
+        return np.where(np.isfinite(v), v, 1.0)
+
+
+def test_interpreter_division_bit_exact_over_the_exponent_range():
+    """x0 / x1 and x1 / x0 (both operand roles of the protected division, and
+    the leaf-pair, accumulator and reversed forms) on 200k cases whose
+    exponents span subnormals to 2^1023: bit-exact with numpy's IEEE
+    division (the device uses an interleaved Newton fast path inside
+    [2^-500, 2^501) and div.rn elsewhere)."""
+    rng = np.random.default_rng(11)
+    n = 200_000
+    X = np.stack([_wide_exponent_values(rng, n), _wide_exponent_values(rng, n)[rng.permutation(n)],
+                  rng.uniform(-1, 1, n)], axis=1)
+    F, V, DIV = int(GeneTag.FUNCTION), int(GeneTag.FEATURE), int(FunctionOp.DIV)
+    progs = [
+        [(V, 0), (V, 1), (F, DIV)],                                  # leaf pair x0 / x1
+        [(V, 1), (V, 0), (F, DIV)],                                  # leaf pair x1 / x0
+        [(V, 0), (V, 2), (V, 2), (F, 0), (F, DIV)],                  # x0 / acc (reversed)
+        [(V, 2), (V, 2), (F, 2), (V, 1), (F, DIV)],                  # acc / x1
+        [(V, 0), (V, 2), (F, 0), (V, 1), (V, 2), (F, 1), (F, DIV)],  # stack / acc
+        [(V, 0), (V, 1), (F, DIV), (V, 1), (V, 0), (F, DIV), (F, DIV)],
+    ]
+    k = max(len(p) for p in progs)
+    tags = np.full((len(progs), k), int(GeneTag.CONSTANT), np.uint8)
+    codes = np.zeros((len(progs), k), np.int32)
+    consts = np.zeros((len(progs), k))
+    for i, p in enumerate(progs):
+        # pad at the front with constants that are dropped (never reach the output)
+        off = k - len(p)
+        consts[i, :off] = 2.5
+        for j, (t, c) in enumerate(p):
+            tags[i, off + j], codes[i, off + j] = t, c
+    S = G.compute_semantics(Population(tags, codes, consts), X, RunConfig(program_size=k))
+    ref, _ = R.semantics(tags, codes, consts, X, 1e-6)
+    assert np.array_equal(S.view(np.uint64), ref.view(np.uint64))
+
+
+def test_interpreter_division_heavy_random_programs_edge_features():
+    rng = np.random.default_rng(5)
+    X = np.stack([_wide_exponent_values(rng, 4099) for _ in range(4)], axis=1)
+    for k in (3, 15, 63, 255, 1024):
+        m = 48
+        tags = rng.choice([0, 0, 1, 2], size=(m, k), p=[0.4, 0.2, 0.3, 0.1]).astype(np.uint8)
+        ops = np.where(rng.random((m, k)) < 0.6, 3, rng.integers(0, 3, (m, k)))
+        codes = np.where(tags == 0, ops, np.where(tags == 1, rng.integers(0, 4, (m, k)), 0)).astype(np.int32)
+        consts = np.where(tags == 2, _wide_exponent_values(rng, m * k).reshape(m, k), 0.0)
+        S = G.compute_semantics(Population(tags, codes, consts), X, RunConfig(program_size=k))
+        ref, _ = R.semantics(tags, codes, consts, X, 1e-6)
+        assert np.array_equal(S.view(np.uint64), ref.view(np.uint64)), k
+
+
 def test_interpreter_many_features_global_path():
     # l = 2000 features exceeds the shared-memory feature tile: global path
     cfg = RunConfig(program_size=255, seed=4)

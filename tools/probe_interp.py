@@ -12,7 +12,8 @@ tr = G.make_benchmark_dataset(c["ntr"], c["l"], seed=1)
 te = G.make_benchmark_dataset(c["nte"], c["l"], seed=2)
 cfg = G.RunConfig(population_size=c["m"], random_trees=c["r"], program_size=c["k"], generations=0, seed=1)
 out = []
-for rep in range(3):
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+for rep in range(reps):
     res = G.run_evolution(cfg, tr, te)
     out.append(round(res.timings.compute_semantics_ms, 2))
 print(json.dumps({"config": cfgname, "compute_semantics_ms": out, "train0": float(res.train_fitness[0])}))
