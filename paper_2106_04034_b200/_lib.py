@@ -7,6 +7,7 @@ compute entry point fails with GsgpError when no CUDA device is present.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
@@ -14,7 +15,9 @@ import numpy as np
 
 from .core import ConfigError, GsgpError
 
-LIB_PATH = Path(__file__).resolve().parent / "libgsgp_b200.so"
+# GSGP_LIB overrides the in-tree build (A/B kernel experiments); either way a
+# missing library is an error, never a fallback
+LIB_PATH = Path(os.environ.get("GSGP_LIB") or Path(__file__).resolve().parent / "libgsgp_b200.so")
 
 _lock = threading.Lock()
 _lib = None

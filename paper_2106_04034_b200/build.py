@@ -25,7 +25,7 @@ HEADERS = ["common.cuh", "kernels.cuh"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CFLAGS = ["-O3", "-std=c++17", "-lineinfo", "-fmad=false", "--expt-relaxed-constexpr",
+CFLAGS = [*os.environ.get("GSGP_NVCC_EXTRA", "").split(), "-O3", "-std=c++17", "-lineinfo", "-fmad=false", "--expt-relaxed-constexpr",
           "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall", "-I", str(ROOT / "include"), "-I", str(CSRC)]
 
 
