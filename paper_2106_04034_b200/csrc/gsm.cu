@@ -41,7 +41,16 @@ __device__ __forceinline__ double mut(double p, double a, double b, double ms, i
 }
 
 // one work unit = (case tile, population row): 16 KB of each streamed row
-constexpr int kTileBytes = 16384;
+#ifndef GSGP_GSM_TILE
+#define GSGP_GSM_TILE 16384
+#endif
+#ifndef GSGP_GSM_STAGES
+#define GSGP_GSM_STAGES 4
+#endif
+#ifndef GSGP_GSM_CWARPS
+#define GSGP_GSM_CWARPS 16
+#endif
+constexpr int kTileBytes = GSGP_GSM_TILE;
 
 // ===================================================================
 // TMA-pipelined persistent kernel (the engine's generation kernel).
@@ -66,9 +75,9 @@ constexpr int kTileBytes = 16384;
 //           unit (fixed warp order) into part[i][t], decoupled from the
 //           consumers through a small mbarrier ring.
 // ===================================================================
-constexpr int kStages = 4;
+constexpr int kStages = GSGP_GSM_STAGES;
 constexpr int kRedStages = 4;
-constexpr int kConsumerWarps = 16;
+constexpr int kConsumerWarps = GSGP_GSM_CWARPS;
 constexpr int kNCT = kConsumerWarps * 32;
 constexpr int kTmaThreads = (kConsumerWarps + 2) * 32;
 
@@ -126,7 +135,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // offspring that equals its parent bit for bit ties with it, as in numpy).
 template <typename T, bool kOp, bool kSseOnly = false>
 __global__ void __launch_bounds__(kTmaThreads, 1)
-k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t nunits) {
+k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t nunits, int kBatch) {
   using Vec = typename Vec16<T>::type;
   constexpr int EV = Vec16<T>::n;
   constexpr int TILE = kTileBytes / (int)sizeof(T);   // elements per unit
@@ -197,11 +206,11 @@ k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t nunits) {
       double* ms_out = const_cast<double*>(ms);
       int s = 0;
       uint32_t j = 0;
-      // tickets are claimed kBatch units at a time, one claim ahead, so the
-      // atomic's round trip overlaps the current units' copies.  (Claiming
-      // several batches ahead and bulk-prefetching their parent tiles into
-      // L2 was measured slower on every config: profiles/r01/README.md.)
-      constexpr int kBatch = 2;
+      // tickets are claimed kBatch units at a time (launch_gsm_mode sizes the
+      // batch to the work per CTA), one claim ahead, so the atomic's round
+      // trip overlaps the current units' copies.  (Claiming several batches
+      // ahead and bulk-prefetching their parent tiles into L2 was measured
+      // slower on every config: profiles/r01/README.md.)
       int64_t next = (int64_t)atomicAdd(a.ticket, (unsigned long long)kBatch);
       int64_t base = 0, t = 0, i = 0;
       int in_batch = kBatch;
@@ -408,9 +417,17 @@ void launch_gsm_mode(const GsmArgs& a, bool f64, int mode, cudaStream_t s) {
   const int64_t nunits = ntiles * a.m;
   const unsigned grid = (unsigned)std::min<int64_t>(g_num_sms, nunits);
   GSGP_REQUIRE(a.ticket != nullptr, "GSM launch needs a ticket counter");
+  // claim size: large batches cut ticket atomics and keep a CTA on
+  // consecutive rows of one tile (C3 0.91 -> 0.97 of peak at 16), but the
+  // last claims of a small launch must still balance across CTAs, so keep
+  // >= 48 claims per CTA (profiles/r01/README.md, batch A/B)
+  static const int forced = getenv("GSGP_GSM_BATCH") ? atoi(getenv("GSGP_GSM_BATCH")) : 0;
+  int batch = 2;
+  while (batch < 16 && nunits / ((int64_t)grid * 2 * batch) >= 48) batch *= 2;
+  if (forced > 0) batch = forced;
   auto go = [&](auto kern) {
     GSGP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
-    kern<<<grid, kTmaThreads, kTmaSmem, s>>>(a, ntiles, nunits);
+    kern<<<grid, kTmaThreads, kTmaSmem, s>>>(a, ntiles, nunits, batch);
   };
   if (f64) {
     if (mode == 1) go(k_gsm_tma<double, true>);
