@@ -20,6 +20,7 @@ from .ops import (
     rng_stream, sample_gene, sigmoid, sigmoid_array, uniform_array,
 )
 from .harness import make_benchmark_dataset, sweep, timed_run
+from .runs import RunSummary, assign_runs, run_many, run_seeds
 from .io_cli import (
     load_config, load_dataset, read_lineage_sidecar, run_cli, write_dataset,
     write_lineage_sidecar, write_traces,
