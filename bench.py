@@ -48,7 +48,10 @@ CONFIGS = {
                desc="C4 pop 8192, 1M+250k cases, pool 1024, k=255 (depth-8 trees)"),
     "c5": dict(m=2048, r=1024, k=1024, l=100, ntr=2_000_000, nte=500_000, g=50,
                desc="C5 pop 2048, 100 features, 2M+500k cases, pool 1024, k=1024"),
-    # profiling shape: C4's population/pool ratio on C2's case count (kernel-replay ncu fits)
+    # profiling shapes: C4's population/pool ratio on C2's case count, C5's feature count on
+    # 200k+50k cases (kernel-replay ncu fits)
+    "c5s": dict(m=2048, r=1024, k=1024, l=100, ntr=200_000, nte=50_000, g=50,
+                desc="C5-shaped profiling config: pop 2048, 100 features, 200k+50k cases"),
     "c4s": dict(m=8192, r=1024, k=255, l=8, ntr=100_000, nte=25_000, g=50,
                 desc="C4-shaped profiling config: pop 8192, pool 1024, k=255, 100k+25k cases"),
 }
