@@ -220,7 +220,9 @@ def run_ours(args):
         e2e = {"value": K / wall, "unit": METRIC, "h2d_bytes_per_step": h2d / K,
                "d2h_bytes_per_step": d2h / K, "wall_s": wall,
                "init_ms": res2.timings.create_population_ms + res2.timings.compute_semantics_ms,
-               "loop_ms": res2.timings.evolution_ms}
+               "loop_ms": res2.timings.evolution_ms,
+               "engine_host_ms": res2.device["engine_total_ms"],
+               "init_phases_ms": res2.device["init_ms"]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -268,7 +270,8 @@ def run_ours(args):
             "gpu_launches": res.device["window_loop_launches"],
             "clocks": clocks,
             "init_ms": {"create_population": res.timings.create_population_ms,
-                        "compute_semantics": res.timings.compute_semantics_ms},
+                        "compute_semantics": res.timings.compute_semantics_ms,
+                        **res.device["init_ms"]},
             "timing_note": "timed run: direct launches with CUDA events around every GSM launch "
                            "on the engine stream (run_evolution(time_kernels=True)); the default "
                            "API path replays one captured generation as a CUDA graph",

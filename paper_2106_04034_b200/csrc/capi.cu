@@ -209,6 +209,8 @@ int gsgp_compute_semantics(const uint8_t* tags, const int32_t* codes, const doub
     a.l = l;
     a.ntr = n;
     a.nte = 0;
+    a.q_base = 0;
+    a.nq = n;
     a.eps = eps;
     a.maxdepth = maxima[0];
     a.maxconst = maxima[1];

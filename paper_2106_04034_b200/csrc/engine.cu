@@ -10,7 +10,9 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -164,6 +166,26 @@ inline unsigned nblk(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t
 }  // namespace
 
 // --------------------------------------------------------------------- run
+// pinned host staging for the chunked case upload, kept for the process
+// lifetime (grown on demand): page-locking a fresh buffer per run would cost
+// more than the copy it enables
+constexpr size_t kUploadChunkBytes = 48u << 20;
+struct PinnedStage {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+PinnedStage& pinned_stage(size_t bytes) {
+  static PinnedStage s;
+  if (s.bytes < bytes) {
+    if (s.p) GSGP_CUDA(cudaFreeHost(s.p));
+    s.p = nullptr;
+    s.bytes = 0;
+    GSGP_CUDA(cudaHostAlloc(&s.p, bytes, cudaHostAllocDefault));
+    s.bytes = bytes;
+  }
+  return s;
+}
+
 struct Shard {
   int64_t tr_lo = 0, tr_hi = 0, te_lo = 0, te_hi = 0;
   int64_t ntr = 0, nte = 0, pitch = 0, test_off = 0, ntiles = 0;
@@ -194,12 +216,14 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   const int W = cs.world;
   const int64_t nsh_total = (int64_t)W * G;
 
-  cudaStream_t st;
+  cudaStream_t st, up;   // compute stream, host->device upload stream
   GSGP_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   struct StreamGuard {
     cudaStream_t s;
     ~StreamGuard() { cudaStreamDestroy(s); }
   } sg{st};
+  GSGP_CUDA(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
+  StreamGuard sg_up{up};
 
   Event ev_begin, ev_created, ev_sem, ev_loop0, ev_loop1;
   GSGP_CUDA(cudaEventRecord(ev_begin.e, st));
@@ -276,6 +300,7 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   GSGP_CUDA(cudaStreamSynchronize(st));
 
   // ---- per shard: upload the case slice, interpret population and pool
+  double init_phase_ms[4] = {0, 0, 0, 0};   // upload, population, pool, initial SSE
   for (auto& p : sh) {
     const int64_t N = p->ntr + p->nte;
     p->S.alloc(m * p->pitch * esz);
@@ -296,22 +321,9 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
     GSGP_CUDA(cudaMemsetAsync(p->y_store.p, 0, p->pitch * 8, st));
     GSGP_CUDA(cudaMemsetAsync(p->sse.p, 0, m * 2 * 8, st));
     if (N == 0) continue;
-    GSGP_CUDA(cudaMemcpyAsync(p->y_store.as<double>(), ytr + p->tr_lo, p->ntr * 8, cudaMemcpyHostToDevice, st));
-    GSGP_CUDA(cudaMemcpyAsync(p->y_store.as<double>() + p->test_off, yte + p->te_lo, p->nte * 8,
-                              cudaMemcpyHostToDevice, st));
-    DevBuf Xr, XT, ystack;
-    Xr.alloc(N * l * 8);
-    XT.alloc(N * l * 8);
-    ystack.alloc(N * 8);
-    GSGP_CUDA(cudaMemcpyAsync(Xr.as<double>(), Xtr + p->tr_lo * l, p->ntr * l * 8, cudaMemcpyHostToDevice, st));
-    GSGP_CUDA(cudaMemcpyAsync(Xr.as<double>() + p->ntr * l, Xte + p->te_lo * l, p->nte * l * 8,
-                              cudaMemcpyHostToDevice, st));
-    GSGP_CUDA(cudaMemcpyAsync(ystack.as<double>(), ytr + p->tr_lo, p->ntr * 8, cudaMemcpyHostToDevice, st));
-    GSGP_CUDA(cudaMemcpyAsync(ystack.as<double>() + p->ntr, yte + p->te_lo, p->nte * 8,
-                              cudaMemcpyHostToDevice, st));
-    k_transpose<<<nblk(N * l), 256, 0, st>>>(Xr.as<double>(), N, l, XT.as<double>());
-    GSGP_CUDA(cudaGetLastError());
-
+    // Cases are uploaded and interpreted in chunks: the host copies chunk c
+    // into a pinned staging buffer while the device interprets chunk c-1, so
+    // the feature upload hides behind the (compute-bound) interpreter.
     InterpArgs ia{};
     ia.code = ins.as<Ins>();
     ia.exe = exe.as<Ins>();
@@ -320,8 +332,6 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
     ia.ctab = ctab.as<double>();
     ia.k1 = k + 1;
     ia.count = m;
-    ia.XT = XT.as<double>();
-    ia.xt_pitch = N;
     ia.l = l;
     ia.ntr = p->ntr;
     ia.nte = p->nte;
@@ -333,15 +343,15 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
     ia.out_is_f64 = f64 ? 1 : 0;
     ia.pitch = p->pitch;
     ia.test_off = p->test_off;
-    ia.y = ystack.as<double>();
+    ia.y = p->y_store.as<double>();
     ia.wide = wide.as<int32_t>();
     ia.nonfinite = nonfinite.as<unsigned long long>();
-    const int64_t itiles = interp_tiles(ia, nullptr);
+    int itile = 1;
+    const int64_t itiles = interp_tiles(ia, &itile);
     DevBuf ipart;
     ipart.alloc(m * itiles * 2 * 8);
     ia.part = ipart.as<double>();
-    launch_interpret(ia, INTERP_POP, st);
-    launch_reduce_partials(ipart.as<double>(), m, itiles, p->sse64.as<double>(), false, st);
+    ia.part_ntiles = itiles;
     // pool: stream base m, same compiled program buffer offset by m genomes
     InterpArgs ip = ia;
     ip.code = ins.as<Ins>() + m * (k + 1);
@@ -354,7 +364,70 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
     ip.part = nullptr;
     ip.wide = nullptr;
     ip.y = nullptr;
-    launch_interpret(ip, INTERP_POOL, st);
+
+    const size_t row_bytes = (size_t)l * 8 + 8;             // features + target of one case
+    int64_t chunk = (int64_t)(kUploadChunkBytes / row_bytes) / 1024 * 1024;
+    if (const char* e = getenv("GSGP_UPLOAD_CHUNK")) chunk = atoll(e) / 1024 * 1024;   // tests
+    if (chunk < 1024) chunk = 1024;                          // multiple of every interpreter tile
+    if (chunk > N) chunk = (N + itile - 1) / itile * itile;
+    const int64_t nchunks = (N + chunk - 1) / chunk;
+    PinnedStage& pin = pinned_stage(2 * (size_t)chunk * row_bytes);
+    DevBuf Xr[2], XT[2];
+    for (int b = 0; b < 2 && b < nchunks; ++b) {
+      Xr[b].alloc(chunk * l * 8);
+      XT[b].alloc(chunk * l * 8);
+    }
+    Event ev_h2d[2], ev_done[2], e_start, e_first;
+    std::vector<std::unique_ptr<Event>> ev_k;
+    GSGP_CUDA(cudaEventRecord(e_start.e, st));
+    for (int64_t c = 0; c < nchunks; ++c) {
+      const int b = (int)(c & 1);
+      const int64_t c0 = c * chunk, nq = std::min(chunk, N - c0);
+      double* hx = reinterpret_cast<double*>(pin.p) + (size_t)b * chunk * (l + 1);
+      double* hy = hx + (size_t)chunk * l;
+      if (c >= 2) GSGP_CUDA(cudaEventSynchronize(ev_h2d[b].e));   // staging buffer b is free
+      // rows [c0, c0 + nq) of the stacked shard (train rows, then test rows)
+      const int64_t ntr_part = std::max<int64_t>(0, std::min(nq, p->ntr - c0));
+      if (ntr_part > 0) {
+        std::memcpy(hx, Xtr + (p->tr_lo + c0) * l, ntr_part * l * 8);
+        std::memcpy(hy, ytr + p->tr_lo + c0, ntr_part * 8);
+      }
+      if (nq > ntr_part) {
+        const int64_t t0 = c0 + ntr_part - p->ntr;          // first test row of the chunk
+        std::memcpy(hx + ntr_part * l, Xte + (p->te_lo + t0) * l, (nq - ntr_part) * l * 8);
+        std::memcpy(hy + ntr_part, yte + p->te_lo + t0, (nq - ntr_part) * 8);
+      }
+      if (c >= 2) GSGP_CUDA(cudaStreamWaitEvent(up, ev_done[b].e, 0));   // device buffers free
+      GSGP_CUDA(cudaMemcpyAsync(Xr[b].p, hx, nq * l * 8, cudaMemcpyHostToDevice, up));
+      if (ntr_part > 0)
+        GSGP_CUDA(cudaMemcpyAsync(p->y_store.as<double>() + c0, hy, ntr_part * 8, cudaMemcpyHostToDevice, up));
+      if (nq > ntr_part)
+        GSGP_CUDA(cudaMemcpyAsync(p->y_store.as<double>() + p->test_off + (c0 + ntr_part - p->ntr),
+                                  hy + ntr_part, (nq - ntr_part) * 8, cudaMemcpyHostToDevice, up));
+      GSGP_CUDA(cudaEventRecord(ev_h2d[b].e, up));
+      GSGP_CUDA(cudaStreamWaitEvent(st, ev_h2d[b].e, 0));
+      k_transpose<<<nblk(nq * l), 256, 0, st>>>(Xr[b].as<double>(), nq, l, XT[b].as<double>());
+      GSGP_CUDA(cudaGetLastError());
+      if (c == 0) GSGP_CUDA(cudaEventRecord(e_first.e, st));
+      for (InterpArgs* q : {&ia, &ip}) {
+        q->XT = XT[b].as<double>();
+        q->xt_pitch = nq;
+        q->q_base = c0;
+        q->nq = nq;
+      }
+      ev_k.push_back(std::make_unique<Event>());
+      GSGP_CUDA(cudaEventRecord(ev_k.back()->e, st));
+      launch_interpret(ia, INTERP_POP, st);
+      ev_k.push_back(std::make_unique<Event>());
+      GSGP_CUDA(cudaEventRecord(ev_k.back()->e, st));
+      launch_interpret(ip, INTERP_POOL, st);
+      ev_k.push_back(std::make_unique<Event>());
+      GSGP_CUDA(cudaEventRecord(ev_k.back()->e, st));
+      GSGP_CUDA(cudaEventRecord(ev_done[b].e, st));
+    }
+    launch_reduce_partials(ipart.as<double>(), m, itiles, p->sse64.as<double>(), false, st);
+    Event e_sse0, e_sse;
+    GSGP_CUDA(cudaEventRecord(e_sse0.e, st));
     // initial SSE of the stored semantics in the generation kernel's order
     GsmArgs ga{};
     ga.pool = p->pool.p;
@@ -369,6 +442,14 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
     ga.ticket = p->ticket.as<unsigned long long>();
     launch_sse_only(ga, f64, st);
     launch_reduce_partials(p->part.as<double>(), m, p->ntiles, p->sse.as<double>(), false, st);
+    GSGP_CUDA(cudaEventRecord(e_sse.e, st));
+    GSGP_CUDA(cudaEventSynchronize(e_sse.e));   // the shard's temporaries are freed at scope end
+    init_phase_ms[0] += elapsed_ms(e_start, e_first);      // exposed upload (first chunk)
+    for (size_t q = 0; q + 2 < ev_k.size(); q += 3) {
+      init_phase_ms[1] += elapsed_ms(*ev_k[q], *ev_k[q + 1]);
+      init_phase_ms[2] += elapsed_ms(*ev_k[q + 1], *ev_k[q + 2]);
+    }
+    init_phase_ms[3] += elapsed_ms(e_sse0, e_sse);
     GSGP_CUDA(cudaStreamSynchronize(st));   // temporaries (Xr, XT, ipart) are freed on scope exit
   }
 
@@ -570,6 +651,7 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   out->stage_ms[9] = win_gsm_ms;
   out->stage_ms[10] = timed ? (double)((g - w0) * gsm_per_gen) : 0.0;
   out->stage_ms[11] = (double)((g - w0) * launches_per_gen);
+  for (int q = 0; q < 4; ++q) out->stage_ms[12 + q] = init_phase_ms[q];
 }
 
 }  // namespace gsgp

@@ -277,15 +277,16 @@ __device__ __forceinline__ uint4 lds_u128(uint32_t p) {
 
 
 template <int NT, int CPT, int MODE, typename TOut, bool kXSmem>
-__global__ void __launch_bounds__(NT) k_interpret(InterpArgs a, int64_t ntiles, int64_t gpb,
+__global__ void __launch_bounds__(NT) k_interpret(InterpArgs a, int64_t gpb,
                                                   uint32_t crow_off, uint32_t prog_off) {
   constexpr int TILE = NT * CPT;
   constexpr uint32_t CSTRIDE = NT * 8;          // bytes between a thread's cases
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x;
   const uint32_t tid8 = (uint32_t)tid * 8u;
-  const int64_t tile = blockIdx.x;
-  const int64_t q0 = tile * TILE;
+  const int64_t tile = blockIdx.x;             // tile of this launch's case range
+  const int64_t l0 = tile * TILE;               // first case of the tile, launch-local
+  const int64_t q0 = a.q_base + l0;             // ... and as a shard stacked index
   const int64_t N = a.ntr + a.nte;
   __shared__ double red[32];
 
@@ -293,8 +294,7 @@ __global__ void __launch_bounds__(NT) k_interpret(InterpArgs a, int64_t ntiles, 
     double* xs = reinterpret_cast<double*>(smem);
     for (int64_t e = tid; e < (int64_t)a.l * TILE; e += NT) {
       const int64_t f = e / TILE, c = e - f * TILE;
-      const int64_t q = q0 + c;
-      xs[e] = q < N ? a.XT[f * a.xt_pitch + q] : 0.0;
+      xs[e] = l0 + c < a.nq ? a.XT[f * a.xt_pitch + l0 + c] : 0.0;
     }
   }
   double ytr[CPT];
@@ -303,12 +303,12 @@ __global__ void __launch_bounds__(NT) k_interpret(InterpArgs a, int64_t ntiles, 
 #pragma unroll
   for (int c = 0; c < CPT; ++c) {
     const int64_t q = q0 + c * NT + tid;
-    valid[c] = q < N;
+    valid[c] = l0 + c * NT + tid < a.nq;
     train[c] = q < a.ntr;
     col[c] = train[c] ? q : a.test_off + (q - a.ntr);
-    ytr[c] = (MODE == INTERP_POP && valid[c]) ? a.y[q] : 0.0;
+    ytr[c] = (MODE == INTERP_POP && valid[c]) ? a.y[col[c]] : 0.0;
   }
-  const double* xg = a.XT + q0 + tid;          // global feature rows (!kXSmem)
+  const double* xg = a.XT + l0 + tid;          // global feature rows (!kXSmem)
   uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
   asm volatile("" : "+r"(sbase));              // keep it in a register (no per-iteration remat)
   const uint32_t pbase = sbase + prog_off;
@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(NT) k_interpret(InterpArgs a, int64_t ntiles, 
       if (tid < 2) {
         double t = 0.0;
         for (int w = 0; w < NT / 32; ++w) t = __dadd_rn(t, red[w * 2 + tid]);
-        a.part[(g * ntiles + tile) * 2 + tid] = t;
+        a.part[(g * a.part_ntiles + a.q_base / TILE + tile) * 2 + tid] = t;
       }
     }
   }
@@ -417,8 +417,8 @@ template <int NT, int CPT, int MODE, typename TOut, bool kXSmem>
 void launch_cfg(const InterpArgs& a, cudaStream_t s) {
   constexpr int TILE = NT * CPT;
   constexpr InterpCfg c{NT, CPT, kXSmem};
-  const int64_t N = a.ntr + a.nte;
-  const int64_t ntiles = (N + TILE - 1) / TILE;
+  const int64_t ntiles = (a.nq + TILE - 1) / TILE;
+  GSGP_REQUIRE(a.q_base % TILE == 0 && a.q_base + a.nq <= a.ntr + a.nte, "bad interpreter case range");
   const uint32_t rowb = TILE * 8;
   const uint32_t frows = kXSmem ? (uint32_t)a.l : 0u;
   const size_t smem = cfg_smem(c, a);
@@ -437,7 +437,7 @@ void launch_cfg(const InterpArgs& a, cudaStream_t s) {
   dim3 grid((unsigned)ntiles, (unsigned)gy);
   auto k = k_interpret<NT, CPT, MODE, TOut, kXSmem>;
   GSGP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k<<<grid, NT, smem, s>>>(a, ntiles, gpb, (frows + (uint32_t)a.maxdepth) * rowb,
+  k<<<grid, NT, smem, s>>>(a, gpb, (frows + (uint32_t)a.maxdepth) * rowb,
                            (uint32_t)cfg_rows_bytes(c, a));
   GSGP_CUDA(cudaGetLastError());
 }
@@ -464,15 +464,15 @@ void launch_compile(const uint8_t* tags, const int32_t* codes, const double* con
   GSGP_CUDA(cudaGetLastError());
 }
 
-int64_t interp_tiles(const InterpArgs& a, int* cpt_out) {
+int64_t interp_tiles(const InterpArgs& a, int* tile_out) {
   const InterpCfg c = kCfgs[choose_cfg(a)];
-  if (cpt_out) *cpt_out = c.cpt;
   const int64_t tile = (int64_t)c.nt * c.cpt;
+  if (tile_out) *tile_out = (int)tile;
   return (a.ntr + a.nte + tile - 1) / tile;
 }
 
 void launch_interpret(const InterpArgs& a, int mode, cudaStream_t s) {
-  if (a.count <= 0 || a.ntr + a.nte <= 0) return;
+  if (a.count <= 0 || a.nq <= 0) return;
   GSGP_REQUIRE(a.maxdepth <= 31, "spill stack deeper than the compiler's labels");
   if (mode == INTERP_F64) launch_mode<INTERP_F64, double>(a, s);
   else if (mode == INTERP_POP) {

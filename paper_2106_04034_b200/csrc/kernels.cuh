@@ -79,10 +79,12 @@ struct InterpArgs {
   int64_t k1;               // instruction stride per genome (k + 1)
   int64_t count;            // genomes
   int32_t maxdepth, maxconst, maxlen;   // Program::maxima, read back once after compile
-  const double* XT;         // [l][ncase_pitch] fp64, feature-major, cases stacked train|test
+  const double* XT;         // [l][xt_pitch] fp64, feature-major: cases q_base .. q_base+nq-1
   int64_t xt_pitch;
   int32_t l;
-  int64_t ntr, nte;         // local case counts (stacked index q < ntr is train)
+  int64_t ntr, nte;         // shard case counts (stacked index q < ntr is train)
+  int64_t q_base, nq;       // this launch: stacked cases [q_base, q_base + nq) (q_base % tile == 0)
+  int64_t part_ntiles;      // row stride of part[] (tiles over all ntr + nte cases)
   double eps;
   // outputs
   double* out64;            // INTERP_F64: [count][ntr+nte]
@@ -90,13 +92,14 @@ struct InterpArgs {
   int32_t out_is_f64;
   int64_t pitch;            // storage pitch (elements); test region starts at test_off
   int64_t test_off;
-  const double* y;          // [ntr+nte] stacked targets (INTERP_POP)
+  const double* y;          // targets in storage layout (pitch, test at test_off) (INTERP_POP)
   double* part;             // [count][ntiles][2] SSE partials (INTERP_POP)
   int32_t* wide;            // [count] bit0 train overflowed fp32, bit1 test (INTERP_POP)
   unsigned long long* nonfinite;   // element count replaced by 0.0
   int32_t raw;              // INTERP_F64 only: keep non-finite values (scalar interpret)
 };
-int64_t interp_tiles(const InterpArgs& a, int* cpt_out);
+// case tiles over all ntr + nte cases (the part[] row stride) and the tile size
+int64_t interp_tiles(const InterpArgs& a, int* tile_out);
 void launch_interpret(const InterpArgs& a, int mode, cudaStream_t s);
 
 // ------------------------------------------------------------ generation
