@@ -69,12 +69,14 @@ typedef struct gsgp_outputs {
   int64_t overflow;              /* out: non-finite replacements (RunStats) */
   int64_t shard_train_lo;        /* out: this rank's train case slice */
   int64_t shard_train_hi;
-  double stage_ms[16];           /* out: 0 create, 1 semantics, 2 evolution, 3 per_generation,
+  double stage_ms[20];           /* out: 0 create, 1 semantics, 2 evolution, 3 per_generation,
                                     4 total (host), 5 gsm_kernel_ms_sum, 6 gsm_launches,
                                     7 loop_launches, 8 window_ms, 9 window_gsm_ms,
                                     10 window_gsm_launches, 11 window_loop_launches,
                                     12 upload (H2D + transpose), 13 interpret population,
-                                    14 interpret pool, 15 initial SSE (sums over shards) */
+                                    14 interpret pool, 15 initial SSE (sums over shards),
+                                    16 genome compile, 17 device allocation + clears (host
+                                    clock), 18-19 reserved */
 } gsgp_outputs;
 
 const char* gsgp_version(void);

@@ -58,7 +58,7 @@ class GsgpOutputs(C.Structure):
         ("gsm_ms", C.c_void_p),
         ("overflow", C.c_int64),
         ("shard_train_lo", C.c_int64), ("shard_train_hi", C.c_int64),
-        ("stage_ms", C.c_double * 16),
+        ("stage_ms", C.c_double * 20),
     ]
 
 

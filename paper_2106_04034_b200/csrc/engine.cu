@@ -293,16 +293,21 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   Program prog{ins.as<Ins>(), exe.as<Ins>(), plen.as<int32_t>(), pnconst.as<int32_t>(),
                ctab.as<double>(), pmax.as<int32_t>(), scratch.as<int32_t>(), flags.as<uint8_t>(),
                cval.as<double>()};
+  Event ev_compile0, ev_compile1;
+  GSGP_CUDA(cudaEventRecord(ev_compile0.e, st));
   launch_compile(tags.as<uint8_t>(), codes.as<int32_t>(), consts.as<double>(), ng, (int32_t)k,
                  cfg->division_eps, prog, st);
+  GSGP_CUDA(cudaEventRecord(ev_compile1.e, st));
   int32_t maxima[3] = {0, 0, 0};   // {spill depth, constants, instructions}
   GSGP_CUDA(cudaMemcpyAsync(maxima, pmax.p, 12, cudaMemcpyDeviceToHost, st));
   GSGP_CUDA(cudaStreamSynchronize(st));
 
   // ---- per shard: upload the case slice, interpret population and pool
   double init_phase_ms[4] = {0, 0, 0, 0};   // upload, population, pool, initial SSE
+  double alloc_ms = 0.0;                     // host clock: device allocations + clears
   for (auto& p : sh) {
     const int64_t N = p->ntr + p->nte;
+    const auto t_alloc0 = std::chrono::steady_clock::now();
     p->S.alloc(m * p->pitch * esz);
     p->pool.alloc(r * p->pitch * esz);
     p->elite[0].alloc(p->pitch * esz);
@@ -320,6 +325,8 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
     GSGP_CUDA(cudaMemsetAsync(p->elite[1].p, 0, p->pitch * esz, st));
     GSGP_CUDA(cudaMemsetAsync(p->y_store.p, 0, p->pitch * 8, st));
     GSGP_CUDA(cudaMemsetAsync(p->sse.p, 0, m * 2 * 8, st));
+    GSGP_CUDA(cudaStreamSynchronize(st));
+    alloc_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_alloc0).count();
     if (N == 0) continue;
     // Cases are uploaded and interpreted in chunks: the host copies chunk c
     // into a pinned staging buffer while the device interprets chunk c-1, so
@@ -652,6 +659,8 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   out->stage_ms[10] = timed ? (double)((g - w0) * gsm_per_gen) : 0.0;
   out->stage_ms[11] = (double)((g - w0) * launches_per_gen);
   for (int q = 0; q < 4; ++q) out->stage_ms[12 + q] = init_phase_ms[q];
+  out->stage_ms[16] = elapsed_ms(ev_compile0, ev_compile1);
+  out->stage_ms[17] = alloc_ms;
 }
 
 }  // namespace gsgp

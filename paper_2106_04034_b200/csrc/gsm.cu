@@ -60,8 +60,9 @@ constexpr int kTileBytes = GSGP_GSM_TILE;
 // case tiles in lockstep and each pool tile is fetched from HBM once, then
 // re-served from L2 to every row that references it (pool copies: L2
 // evict_last; parent: evict_first; offspring stores: streaming).
-//   warp 8  producer (one lane): claims units, draws the row's mutation plan
-//           (u, v, ms) from the counter RNG, and issues 3 cp.async.bulk
+//   warp 8  producer: claims batches of units, the warp's lanes draw the
+//           rows' mutation plans (u, v, ms) from the counter RNG in
+//           parallel, and one lane issues 3 cp.async.bulk
 //           copies (parent row tile, pool[u] tile, pool[v] tile) into a
 //           kStages-deep shared-memory ring; completion = mbarrier
 //           transaction count.
@@ -198,68 +199,84 @@ k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t nunits, int kBatch) {
   // -1 terminates the consumers, who forward it to the finalizer.
   if (warp == kConsumerWarps) {
     // ------------------------------------------------------------ producer
-    if (lane == 0) {
-      const uint64_t keep = l2_policy_evict_last(), stream = l2_policy_evict_first();
-      const uint64_t plan_key = stream_key(a.plan.seed, kPlanStream0 + (uint64_t)gen);
-      int64_t* u_out = const_cast<int64_t*>(u);
-      int64_t* v_out = const_cast<int64_t*>(vv);
-      double* ms_out = const_cast<double*>(ms);
-      int s = 0;
-      uint32_t j = 0;
-      // tickets are claimed kBatch units at a time (launch_gsm_mode sizes the
-      // batch to the work per CTA), one claim ahead, so the atomic's round
-      // trip overlaps the current units' copies.  (Claiming several batches
-      // ahead and bulk-prefetching their parent tiles into L2 was measured
-      // slower on every config: profiles/r01/README.md.)
-      int64_t next = (int64_t)atomicAdd(a.ticket, (unsigned long long)kBatch);
-      int64_t base = 0, t = 0, i = 0;
-      int in_batch = kBatch;
-      for (int64_t k = 0;; ++k) {
-        if (in_batch == kBatch) {
-          base = next;
-          if (base < nunits) next = (int64_t)atomicAdd(a.ticket, (unsigned long long)kBatch);
-          in_batch = 0;
-          t = base / m;                 // one division per claimed batch
-          i = base - t * m;
-        } else if (++i == m) {          // next unit of the batch: next row (or tile)
-          i = 0;
-          ++t;
-        }
-        const int64_t unit = base + in_batch++;
-        if (k >= kStages) mbar_wait(empty + s, (j & 1) ^ 1);
-        if (unit >= nunits) {
-          slot_unit[s] = -1;
-          mbar_arrive(full + s);
-          break;
-        }
-        const int64_t off = t * TILE;
-        const int64_t n = min((int64_t)TILE, a.pitch - off);
-        int64_t ui = 0, vi = 0;
-        double msd = 0.0;
+    // The whole warp produces: when a batch of units is claimed, lane b
+    // draws the plan of unit base + b (the counter RNG makes every draw
+    // independent), so the per-unit RNG latency is paid once per batch and in
+    // parallel; lane 0 then publishes the units one stage at a time, taking
+    // (row, tile, u, v, ms) from the owning lane with shuffles.
+    const uint64_t keep = l2_policy_evict_last(), stream = l2_policy_evict_first();
+    const uint64_t plan_key = stream_key(a.plan.seed, kPlanStream0 + (uint64_t)gen);
+    int64_t* u_out = const_cast<int64_t*>(u);
+    int64_t* v_out = const_cast<int64_t*>(vv);
+    double* ms_out = const_cast<double*>(ms);
+    int s = 0;
+    uint32_t j = 0;
+    // tickets are claimed kBatch units at a time (launch_gsm_mode sizes the
+    // batch to the work per CTA, <= 32), one claim ahead, so the atomic's
+    // round trip overlaps the current units' copies.  (Claiming several
+    // batches ahead and bulk-prefetching their parent tiles into L2 was
+    // measured slower on every config: profiles/r01/README.md.)
+    int64_t next = 0;
+    if (lane == 0) next = (int64_t)atomicAdd(a.ticket, (unsigned long long)kBatch);
+    next = __shfl_sync(0xffffffffu, next, 0);
+    int64_t k = 0;
+    for (bool done = false; !done;) {
+      const int64_t base = next;
+      if (base < nunits) {
+        if (lane == 0) next = (int64_t)atomicAdd(a.ticket, (unsigned long long)kBatch);
+        next = __shfl_sync(0xffffffffu, next, 0);
+      }
+      // this lane's unit of the batch: (tile tb, row ib)
+      const int64_t ub_unit = base + lane;
+      int64_t tb = 0, ib = 0, ub = 0, vb = 0;
+      double msb = 0.0;
+      if (lane < kBatch && ub_unit < nunits) {
+        tb = ub_unit / m;
+        ib = ub_unit - tb * m;
         if (kSseOnly) {
         } else if (a.plan_inline) {
-          plan_slot(plan_key, i, a.plan.r, a.plan.ms_uniform, a.plan.ms_const, &ui, &vi, &msd);
-          if (t == 0 && a.write_plan) { u_out[i] = ui; v_out[i] = vi; ms_out[i] = msd; }
+          plan_slot(plan_key, ib, a.plan.r, a.plan.ms_uniform, a.plan.ms_const, &ub, &vb, &msb);
+          if (tb == 0 && a.write_plan) { u_out[ib] = ub; v_out[ib] = vb; ms_out[ib] = msb; }
         } else {
-          ui = u[i];
-          vi = vv[i];
-          msd = ms[i];
+          ub = u[ib];
+          vb = vv[ib];
+          msb = ms[ib];
         }
-        const T* src = (i == redirect) ? elite_prev : S + i * a.pitch;
-        const uint32_t bytes = (uint32_t)(n * sizeof(T));
-        T* d = data + (int64_t)s * 3 * TILE;
-        slot_unit[s] = unit;
-        slot_ms[s] = msd;
-        slot_it[s] = make_int2((int)i, (int)t);
-        mbar_expect_tx(full + s, (kSseOnly ? 1 : 3) * bytes);
-        bulk_g2s(d, src + off, bytes, full + s, stream);
-        if (!kSseOnly) {
-          bulk_g2s(d + TILE, pool + ui * a.pitch + off, bytes, full + s, keep);
-          bulk_g2s(d + 2 * TILE, pool + vi * a.pitch + off, bytes, full + s, keep);
+      }
+      for (int q = 0; q < kBatch; ++q, ++k) {
+        const int64_t unit = base + q;
+        const int64_t t = __shfl_sync(0xffffffffu, tb, q), i = __shfl_sync(0xffffffffu, ib, q);
+        const int64_t ui = __shfl_sync(0xffffffffu, ub, q), vi = __shfl_sync(0xffffffffu, vb, q);
+        const double msd = __shfl_sync(0xffffffffu, msb, q);
+        if (lane == 0) {
+          if (k >= kStages) mbar_wait(empty + s, (j & 1) ^ 1);
+          if (unit >= nunits) {
+            slot_unit[s] = -1;
+            mbar_arrive(full + s);
+          } else {
+            const int64_t off = t * TILE;
+            const int64_t n = min((int64_t)TILE, a.pitch - off);
+            const T* src = (i == redirect) ? elite_prev : S + i * a.pitch;
+            const uint32_t bytes = (uint32_t)(n * sizeof(T));
+            T* d = data + (int64_t)s * 3 * TILE;
+            slot_unit[s] = unit;
+            slot_ms[s] = msd;
+            slot_it[s] = make_int2((int)i, (int)t);
+            mbar_expect_tx(full + s, (kSseOnly ? 1 : 3) * bytes);
+            bulk_g2s(d, src + off, bytes, full + s, stream);
+            if (!kSseOnly) {
+              bulk_g2s(d + TILE, pool + ui * a.pitch + off, bytes, full + s, keep);
+              bulk_g2s(d + 2 * TILE, pool + vi * a.pitch + off, bytes, full + s, keep);
+            }
+          }
         }
+        __syncwarp();
+        if (unit >= nunits) { done = true; break; }
         if (++s == kStages) { s = 0; ++j; }
       }
-      // every claim of this CTA is done; the last CTA out re-arms the ticket
+    }
+    // every claim of this CTA is done; the last CTA out re-arms the ticket
+    if (lane == 0) {
       __threadfence();
       if (atomicAdd(a.ticket + 1, 1ull) == (unsigned long long)gridDim.x - 1) {
         atomicExch(a.ticket, 0ull);
@@ -424,7 +441,7 @@ void launch_gsm_mode(const GsmArgs& a, bool f64, int mode, cudaStream_t s) {
   static const int forced = getenv("GSGP_GSM_BATCH") ? atoi(getenv("GSGP_GSM_BATCH")) : 0;
   int batch = 2;
   while (batch < 16 && nunits / ((int64_t)grid * 2 * batch) >= 48) batch *= 2;
-  if (forced > 0) batch = forced;
+  if (forced > 0) batch = forced < 32 ? forced : 32;   // one unit per producer lane
   auto go = [&](auto kern) {
     GSGP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
     kern<<<grid, kTmaThreads, kTmaSmem, s>>>(a, ntiles, nunits, batch);

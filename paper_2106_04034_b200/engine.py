@@ -122,7 +122,8 @@ def run_evolution(cfg: RunConfig, train: Dataset, test: Dataset, *, storage: str
               "gsm_ms_per_generation": a["gsm_ms"][:g] if time_kernels else None,
               "shard_train_range": (int(out.shard_train_lo), int(out.shard_train_hi)),
               "init_ms": {"upload": st[12], "interpret_population": st[13],
-                          "interpret_pool": st[14], "initial_sse": st[15]},
+                          "interpret_pool": st[14], "initial_sse": st[15], "compile": st[16],
+                          "alloc": st[17]},
               "storage": storage}
     return RunResult(
         config=cfg, train_fitness=a["train_trace"], test_fitness=a["test_trace"], lineage=log,
