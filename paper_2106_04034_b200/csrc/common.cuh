@@ -96,11 +96,13 @@ struct __align__(16) Ins {
   // linked (interpret): a = kind | y-is-vector << 8, b = x byte offset,
   //                     c = y byte offset (L*) or push-slot byte offset (PUSHLOAD),
   //                     d = x lane mask (~0 vector row, 0 broadcast constant);
-  //                     feature offsets carry kFeatGlobal when features stay in HBM
+  //                     feature offsets carry kFeatGlobal when features stay in HBM,
+  //                     constants kConstGlobal in the lean (huge-program) configuration
   uint32_t a, b, c, d;
 };
 static_assert(sizeof(Ins) == 16, "Ins must be 16 bytes");
 constexpr uint32_t kFeatGlobal = 0x80000000u;
+constexpr uint32_t kConstGlobal = 0x40000000u;   // lean configuration: constant j read from HBM
 
 // binary op with the reference's protected division (interpreter.py:58-65):
 // each case rounds exactly once, as numpy does.

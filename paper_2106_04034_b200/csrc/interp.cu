@@ -200,31 +200,36 @@ __global__ void k_compile(const uint8_t* __restrict__ tags, const int32_t* __res
 // holds [features][spill slots][constant rows] of the block's case tile.
 struct InterpCfg {
   int nt, cpt;
-  bool xsmem;
+  bool xsmem;   // features of the tile in shared memory (else read from HBM/L2)
+  bool lean;    // program and constants stay in HBM: only the spill rows use
+                // shared memory, so any program size fits (huge k fallback)
 };
-constexpr InterpCfg kCfgs[] = {{128, 4, true}, {64, 8, true}, {128, 4, false},
-                               {128, 2, true}, {128, 1, false}, {64, 8, false}};
+constexpr InterpCfg kCfgs[] = {{128, 4, true, false}, {64, 8, true, false}, {128, 4, false, false},
+                               {128, 2, true, false}, {128, 1, false, true}};
 constexpr int kNumCfgs = sizeof(kCfgs) / sizeof(kCfgs[0]);
 constexpr size_t kSmemCap = 200 * 1024;
 
 // rows of the case tile + the staged program (16 B per instruction)
 size_t cfg_rows_bytes(const InterpCfg& c, const InterpArgs& a) {
   const size_t rowb = (size_t)c.nt * c.cpt * 8;
-  const size_t crows = ((size_t)(a.maxconst > 0 ? a.maxconst : 1) + c.nt - 1) / c.nt;
+  const size_t crows = c.lean ? 0 : ((size_t)(a.maxconst > 0 ? a.maxconst : 1) + c.nt - 1) / c.nt;
   return ((c.xsmem ? (size_t)a.l : 0) + (size_t)a.maxdepth + crows) * rowb;
 }
 size_t cfg_smem(const InterpCfg& c, const InterpArgs& a) {
+  if (c.lean) return cfg_rows_bytes(c, a) + 16;
   // + 1 instruction: the loop prefetches one past the end of the program
   return cfg_rows_bytes(c, a) + (size_t)((a.maxlen > 0 ? a.maxlen : 1) + 1) * sizeof(Ins);
 }
 
 int choose_cfg(const InterpArgs& a) {
-  static const int forced = getenv("GSGP_INTERP_CFG") ? atoi(getenv("GSGP_INTERP_CFG")) : -1;
+  const char* env = getenv("GSGP_INTERP_CFG");   // experiments / tests (read per launch)
+  const int forced = env ? atoi(env) : -1;
   if (forced >= 0 && forced < kNumCfgs && cfg_smem(kCfgs[forced], a) <= kSmemCap) return forced;
   // features in shared memory while the tile keeps >= 3 blocks per SM
   if (cfg_smem(kCfgs[0], a) <= 72 * 1024) return 0;
   if (cfg_smem(kCfgs[2], a) <= 72 * 1024) return 2;
-  return 4;   // 1 KB rows: always fits (depth <= 31, constants <= k)
+  if (cfg_smem(kCfgs[2], a) <= kSmemCap) return 2;
+  return 4;   // lean: spill rows only (depth <= 31 x 1 KB)
 }
 
 // ---------------------------------------------------------------- link
@@ -233,7 +238,7 @@ int choose_cfg(const InterpArgs& a) {
 // (constant j: row j / nt, lane j % nt, replicated for the CPT cases)
 __global__ void k_link(const Ins* __restrict__ code, Ins* __restrict__ exe, const int32_t* __restrict__ len,
                        int64_t count, int64_t k1, int32_t nt, uint32_t rowb, uint32_t frows,
-                       uint32_t maxdepth) {
+                       uint32_t maxdepth, bool lean) {
   const int64_t g = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;   // one warp per genome
   if (g >= count) return;
   const int32_t n = len[g];
@@ -243,6 +248,7 @@ __global__ void k_link(const Ins* __restrict__ code, Ins* __restrict__ exe, cons
     if (cls == X_FEAT) return frows ? idx * rowb : (kFeatGlobal | idx);
     if (cls == X_STACK) return (frows + idx) * rowb;
     vec = 0;
+    if (lean) return kConstGlobal | idx;
     return (frows + maxdepth + idx / (uint32_t)nt) * rowb + (idx % (uint32_t)nt) * 8u;
   };
   for (int32_t i = threadIdx.x % 32; i < n; i += 32) {
@@ -276,7 +282,7 @@ __device__ __forceinline__ uint4 lds_u128(uint32_t p) {
 }
 
 
-template <int NT, int CPT, int MODE, typename TOut, bool kXSmem>
+template <int NT, int CPT, int MODE, typename TOut, bool kXSmem, bool kLean>
 __global__ void __launch_bounds__(NT) k_interpret(InterpArgs a, int64_t gpb,
                                                   uint32_t crow_off, uint32_t prog_off) {
   constexpr int TILE = NT * CPT;
@@ -317,8 +323,13 @@ __global__ void __launch_bounds__(NT) k_interpret(InterpArgs a, int64_t gpb,
 
   // operand fetch: a shared-memory row / broadcast constant, or (features
   // left in HBM) a coalesced global row
+  const double* cg = nullptr;                  // constants of the genome (kLean)
   auto fetch = [&](uint32_t off, uint32_t mask, double (&v)[CPT]) {
-    if (!kXSmem && (off & kFeatGlobal)) {
+    if (kLean && (off & kConstGlobal)) {
+      const double cv = __ldg(cg + (off & ~kConstGlobal));
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) v[c] = cv;
+    } else if (!kXSmem && (off & kFeatGlobal)) {
       const double* p = xg + (int64_t)(off & ~kFeatGlobal) * a.xt_pitch;
 #pragma unroll
       for (int c = 0; c < CPT; ++c) v[c] = valid[c] ? __ldg(p + c * NT) : 0.0;
@@ -335,7 +346,9 @@ __global__ void __launch_bounds__(NT) k_interpret(InterpArgs a, int64_t gpb,
     // ---- stage genome g: program + constant table (replicated for the CPT
     // cases of a thread) into shared memory
     const int len = a.len[g];
-    __syncthreads();                            // previous genome done with both
+    cg = a.ctab + g * cstride;
+    __syncthreads();                            // previous genome done with both (and red[])
+    if (!kLean) {
     {
       const uint4* src = reinterpret_cast<const uint4*>(a.exe + g * a.k1);
       uint4* dst = reinterpret_cast<uint4*>(smem + prog_off);
@@ -349,14 +362,17 @@ __global__ void __launch_bounds__(NT) k_interpret(InterpArgs a, int64_t gpb,
       }
     }
     __syncthreads();
+    }
 
     double acc[CPT];
 #pragma unroll
     for (int c = 0; c < CPT; ++c) acc[c] = 0.0;
-    uint4 nxt = lds_u128(pbase);
+    const uint4* gprog = reinterpret_cast<const uint4*>(a.exe + g * a.k1);   // kLean
+    uint4 nxt = kLean ? __ldg(gprog) : lds_u128(pbase);
     for (int i = 0; i < len; ++i) {
       const uint4 in = nxt;
-      nxt = lds_u128(pbase + (uint32_t)(i + 1) * 16u);   // next instruction (smem holds len + 1)
+      // next instruction (smem holds len + 1; the HBM program has k + 1 >= len + 1 slots)
+      nxt = kLean ? __ldg(gprog + i + 1) : lds_u128(pbase + (uint32_t)(i + 1) * 16u);
       double x[CPT];
       fetch(in.y, in.w, x);
       const uint32_t kind = in.x & 0xff;
@@ -413,10 +429,10 @@ __global__ void __launch_bounds__(NT) k_interpret(InterpArgs a, int64_t gpb,
   if ((tid & 31) == 0 && nonfinite) atomicAdd(a.nonfinite, nonfinite);
 }
 
-template <int NT, int CPT, int MODE, typename TOut, bool kXSmem>
+template <int NT, int CPT, int MODE, typename TOut, bool kXSmem, bool kLean = false>
 void launch_cfg(const InterpArgs& a, cudaStream_t s) {
   constexpr int TILE = NT * CPT;
-  constexpr InterpCfg c{NT, CPT, kXSmem};
+  constexpr InterpCfg c{NT, CPT, kXSmem, kLean};
   const int64_t ntiles = (a.nq + TILE - 1) / TILE;
   GSGP_REQUIRE(a.q_base % TILE == 0 && a.q_base + a.nq <= a.ntr + a.nte, "bad interpreter case range");
   const uint32_t rowb = TILE * 8;
@@ -425,7 +441,7 @@ void launch_cfg(const InterpArgs& a, cudaStream_t s) {
   GSGP_REQUIRE(smem <= kSmemCap, "interpreter tile does not fit in shared memory");
   // link the programs for this row layout
   k_link<<<(unsigned)((a.count + 3) / 4), 128, 0, s>>>(a.code, a.exe, a.len, a.count, a.k1, NT, rowb,
-                                                      frows, (uint32_t)a.maxdepth);
+                                                      frows, (uint32_t)a.maxdepth, kLean);
   GSGP_CUDA(cudaGetLastError());
   // genomes per block: enough blocks to fill 148 SMs several times over
   const int64_t want = 148 * 8;
@@ -435,7 +451,7 @@ void launch_cfg(const InterpArgs& a, cudaStream_t s) {
   const int64_t gy = (a.count + gpb - 1) / gpb;
   GSGP_REQUIRE(gy <= 65535, "too many genome groups");
   dim3 grid((unsigned)ntiles, (unsigned)gy);
-  auto k = k_interpret<NT, CPT, MODE, TOut, kXSmem>;
+  auto k = k_interpret<NT, CPT, MODE, TOut, kXSmem, kLean>;
   GSGP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k<<<grid, NT, smem, s>>>(a, gpb, (frows + (uint32_t)a.maxdepth) * rowb,
                            (uint32_t)cfg_rows_bytes(c, a));
@@ -449,8 +465,7 @@ void launch_mode(const InterpArgs& a, cudaStream_t s) {
     case 1: launch_cfg<64, 8, MODE, TOut, true>(a, s); break;
     case 2: launch_cfg<128, 4, MODE, TOut, false>(a, s); break;
     case 3: launch_cfg<128, 2, MODE, TOut, true>(a, s); break;
-    case 4: launch_cfg<128, 1, MODE, TOut, false>(a, s); break;
-    default: launch_cfg<64, 8, MODE, TOut, false>(a, s); break;
+    default: launch_cfg<128, 1, MODE, TOut, false, true>(a, s); break;
   }
 }
 

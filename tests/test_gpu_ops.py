@@ -335,3 +335,23 @@ def test_survive_state_copy():
     assert (e.source, e.index, e.slot) == ("parent", 1, 3)
     assert np.array_equal(nxt.train_semantics[3], parent.train_semantics[1])
     assert nxt.fitness[3] == 0.5
+
+
+def test_interpreter_lean_configuration_matches(monkeypatch):
+    """The lean launch configuration (program and constants read from HBM,
+    only spill rows in shared memory: the fallback for programs too large to
+    stage) gives bit-identical semantics, with many constants per genome."""
+    rng = np.random.default_rng(9)
+    X = rng.uniform(-2, 2, (700, 5))
+    k, m = 511, 16
+    tags = rng.choice([0, 1, 2], size=(m, k), p=[0.5, 0.2, 0.3]).astype(np.uint8)
+    codes = np.where(tags == 0, rng.integers(0, 4, (m, k)),
+                     np.where(tags == 1, rng.integers(0, 5, (m, k)), 0)).astype(np.int32)
+    consts = np.where(tags == 2, rng.uniform(1, 10, (m, k)), 0.0)
+    pop = Population(tags, codes, consts)
+    ref, _ = R.semantics(tags, codes, consts, X, 1e-6)
+    a = G.compute_semantics(pop, X, RunConfig(program_size=k))
+    monkeypatch.setenv("GSGP_INTERP_CFG", "4")
+    b = G.compute_semantics(pop, X, RunConfig(program_size=k))
+    assert np.array_equal(a.view(np.uint64), ref.view(np.uint64))
+    assert np.array_equal(b.view(np.uint64), ref.view(np.uint64))
