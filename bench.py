@@ -222,6 +222,7 @@ def run_ours(args):
                "init_ms": res2.timings.create_population_ms + res2.timings.compute_semantics_ms,
                "loop_ms": res2.timings.evolution_ms,
                "engine_host_ms": res2.device["engine_total_ms"],
+               "engine_call_ms": res2.device["call_ms"], "api_prep_ms": res2.device["prep_ms"],
                "init_phases_ms": res2.device["init_ms"]}
 
     cpu = None

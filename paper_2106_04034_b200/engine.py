@@ -101,8 +101,10 @@ def run_evolution(cfg: RunConfig, train: Dataset, test: Dataset, *, storage: str
     )
     for name, arr in arrays.items():
         setattr(out, name, ptr(arr))
+    t_call = t_call_start = time.perf_counter()
     check(_lib.load().gsgp_run(C.byref(s), ptr(Xtr), ptr(ytr), train.n_cases, ptr(Xte), ptr(yte),
                                test.n_cases, train.n_features, C.byref(out)))
+    t_call = (time.perf_counter() - t_call) * 1e3
     a = arrays
     log = LineageLog(EliteRecord("initial", int(a["elite_idx"][0]), int(a["elite_slot"][0]),
                                  float(a["elite_fit"][0])))
@@ -116,7 +118,8 @@ def run_evolution(cfg: RunConfig, train: Dataset, test: Dataset, *, storage: str
     timings = StageTimings(create_population_ms=st[0], compute_semantics_ms=st[1],
                            evolution_ms=st[2], per_generation_ms=st[3], total_ms=total_ms)
     device = {"stage_ms": st, "gsm_kernel_ms": st[5], "gsm_launches": int(st[6]),
-              "loop_launches": int(st[7]), "engine_total_ms": st[4],
+              "loop_launches": int(st[7]), "engine_total_ms": st[4], "call_ms": t_call,
+              "prep_ms": (t_call_start - t0) * 1e3,
               "window_ms": st[8], "window_gsm_ms": st[9], "window_gsm_launches": int(st[10]),
               "window_loop_launches": int(st[11]),
               "gsm_ms_per_generation": a["gsm_ms"][:g] if time_kernels else None,
