@@ -16,8 +16,9 @@ from .core import (
 from .engine import GenerationState, RunResult, replay_lineage, run_evolution, survive
 from .ops import (
     argmax_fitness, argmin_fitness, build_mutation_plan, compute_fitness, compute_semantics,
-    create_population, derive_seed, gsm, gsm_paired, gsm_step_f32, interpret, rmse, rng_bits,
-    rng_stream, sample_gene, sigmoid, sigmoid_array, uniform_array,
+    create_population, derive_seed, gsm, gsm_paired, gsm_step_f32, interpret,
+    release_device_memory, rmse, rng_bits, rng_stream, sample_gene, sigmoid, sigmoid_array,
+    uniform_array,
 )
 from .harness import make_benchmark_dataset, sweep, timed_run
 from .runs import RunSummary, assign_runs, run_many, run_seeds

@@ -25,7 +25,7 @@ _lib = None
 GSGP_OK, GSGP_ERR_CONFIG, GSGP_ERR_CUDA, GSGP_ERR_NCCL, GSGP_ERR_OOM = range(5)
 
 EXPORTS = (
-    "gsgp_version", "gsgp_last_error", "gsgp_device_info", "gsgp_set_device", "gsgp_rng_draw",
+    "gsgp_version", "gsgp_last_error", "gsgp_device_info", "gsgp_set_device", "gsgp_trim_device_memory", "gsgp_rng_draw",
     "gsgp_derive_seed", "gsgp_create_population", "gsgp_compute_semantics", "gsgp_compute_fitness",
     "gsgp_build_mutation_plan", "gsgp_gsm", "gsgp_gsm_step_f32", "gsgp_survive", "gsgp_run",
     "gsgp_comm_unique_id", "gsgp_comm_init", "gsgp_comm_destroy", "gsgp_shard_range",
@@ -73,6 +73,7 @@ _SIGS = {
     "gsgp_last_error": (C.c_char_p, []),
     "gsgp_device_info": (C.c_int, [P, P, C.c_char_p, C.c_int]),
     "gsgp_set_device": (C.c_int, [C.c_int]),
+    "gsgp_trim_device_memory": (C.c_int, []),
     "gsgp_rng_draw": (C.c_int, [U64, U64, P, I64, P, P]),
     "gsgp_derive_seed": (U64, [U64, U64]),
     "gsgp_create_population": (C.c_int, [C.POINTER(GsgpConfig), I64, U64, I32, P, P, P]),

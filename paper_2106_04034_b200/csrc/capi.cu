@@ -123,6 +123,18 @@ int gsgp_set_device(int device) {
   });
 }
 
+int gsgp_trim_device_memory(void) {
+  return guarded([&] {
+    require_device();
+    int dev = 0;
+    GSGP_CUDA(cudaGetDevice(&dev));
+    cudaMemPool_t pool;
+    GSGP_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    GSGP_CUDA(cudaDeviceSynchronize());
+    GSGP_CUDA(cudaMemPoolTrimTo(pool, 0));
+  });
+}
+
 int gsgp_rng_draw(uint64_t seed, uint64_t stream, const uint64_t* counters, int64_t n, uint64_t* bits,
                   double* units) {
   return guarded([&] {

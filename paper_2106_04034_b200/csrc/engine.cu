@@ -23,24 +23,47 @@
 namespace gsgp {
 
 // ------------------------------------------------------------- device memory
+// Engine buffers come from the device's stream-ordered memory pool on the
+// engine stream (cudaMallocAsync / cudaFreeAsync).  The pool keeps its memory
+// between runs (release threshold = max), so a job's second run allocates
+// and frees its ~100 GB working set without driver calls — a plain cudaFree
+// of a 51 GB buffer was measured at up to 1.6 s.  gsgp_trim_device_memory()
+// hands the pool's memory back.
+thread_local cudaStream_t g_alloc_stream = nullptr;
+
+void configure_pool_once() {
+  static bool done = false;
+  if (done) return;
+  int dev = 0;
+  GSGP_CUDA(cudaGetDevice(&dev));
+  cudaMemPool_t pool;
+  GSGP_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  uint64_t keep = UINT64_MAX;
+  GSGP_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  done = true;
+}
+
 struct DevBuf {
   void* p = nullptr;
+  cudaStream_t s = nullptr;
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
   ~DevBuf() { release(); }
   void release() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, s);
     p = nullptr;
   }
   void alloc(size_t bytes) {
     release();
     if (bytes == 0) bytes = 16;
-    cudaError_t e = cudaMalloc(&p, bytes);
+    s = g_alloc_stream;
+    cudaError_t e = cudaMallocAsync(&p, bytes, s);
     if (e != cudaSuccess) {
+      p = nullptr;
       cudaGetLastError();
       throw Error{e == cudaErrorMemoryAllocation ? ERR_OOM : ERR_CUDA,
-                  "cudaMalloc(" + std::to_string(bytes) + " bytes): " + cudaGetErrorString(e)};
+                  "cudaMallocAsync(" + std::to_string(bytes) + " bytes): " + cudaGetErrorString(e)};
     }
   }
   template <typename T> T* as() const { return reinterpret_cast<T*>(p); }
@@ -224,6 +247,12 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   } sg{st};
   GSGP_CUDA(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
   StreamGuard sg_up{up};
+  configure_pool_once();
+  struct AllocStream {            // DevBufs of this run allocate/free on st
+    cudaStream_t prev;
+    explicit AllocStream(cudaStream_t s) : prev(g_alloc_stream) { g_alloc_stream = s; }
+    ~AllocStream() { g_alloc_stream = prev; }
+  } alloc_stream{st};
 
   Event ev_begin, ev_created, ev_sem, ev_loop0, ev_loop1;
   GSGP_CUDA(cudaEventRecord(ev_begin.e, st));
@@ -384,7 +413,9 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
       Xr[b].alloc(chunk * l * 8);
       XT[b].alloc(chunk * l * 8);
     }
-    Event ev_h2d[2], ev_done[2], e_start, e_first;
+    Event ev_h2d[2], ev_done[2], e_start, e_first, ev_alloc;
+    GSGP_CUDA(cudaEventRecord(ev_alloc.e, st));        // pool allocations are ordered on st
+    GSGP_CUDA(cudaStreamWaitEvent(up, ev_alloc.e, 0));
     std::vector<std::unique_ptr<Event>> ev_k;
     GSGP_CUDA(cudaEventRecord(e_start.e, st));
     for (int64_t c = 0; c < nchunks; ++c) {

@@ -78,6 +78,12 @@ def uniform_array(seed: int, stream: int, counters: np.ndarray) -> np.ndarray:
     return out
 
 
+def release_device_memory() -> None:
+    """Hand the engine's cached device memory back to the driver (runs keep
+    their working set in a stream-ordered pool for the next run)."""
+    check(_lib.load().gsgp_trim_device_memory())
+
+
 def derive_seed(seed: int, index: int) -> int:
     """gsgp/rng.py:67-69."""
     return int(_lib.load().gsgp_derive_seed(u64(seed), u64(index)))
