@@ -78,23 +78,27 @@ enum FunctionOp : int32_t { OP_ADD = 0, OP_SUB = 1, OP_MUL = 2, OP_DIV = 3 };   
 // Sethi-Ullman ordered) genome for the accumulator machine of interp.cu.
 // Every instruction reads one operand x (a feature, a constant-table entry
 // or a static spill-stack slot) and combines it with the accumulator; a
-// node with two leaf children reads a second leaf y instead:
+// node with two leaf children reads a second leaf y instead, and when it
+// starts the second subtree of a spill (the common case: a spill is always
+// followed by such a node) the spill is fused in (P* kinds):
 //   ADD acc+x  SUB acc-x  MUL acc*x  DIV |x|<eps ? 1 : acc/x
 //   RSUB x-acc RDIV |acc|<eps ? 1 : x/acc  LOAD acc=x  PUSHLOAD slot=acc, acc=x
 //   LADD x+y   LSUB x-y   LMUL x*y   LDIV |y|<eps ? 1 : x/y
+//   PADD..PDIV slot=acc, then acc = x op y
 // k_compile emits the abstract form (operand class + index); k_link rewrites
 // it for one interpreter configuration into shared-memory byte offsets, so
 // the interpreter fetches x with one address computation and branches once.
 enum InsKind : uint32_t { K_ADD = 0, K_SUB = 1, K_MUL = 2, K_DIV = 3, K_RSUB = 4, K_RDIV = 5,
                           K_LOAD = 6, K_PUSHLOAD = 7, K_LADD = 8, K_LSUB = 9, K_LMUL = 10,
-                          K_LDIV = 11, K_NUM_KINDS = 12 };
+                          K_LDIV = 11, K_PADD = 12, K_PSUB = 13, K_PMUL = 14, K_PDIV = 15,
+                          K_NUM_KINDS = 16 };
 enum InsClass : uint32_t { X_FEAT = 0, X_CONST = 1, X_STACK = 2 };
 
 struct __align__(16) Ins {
   // abstract (compile): a = kind | x class << 8 | y class << 12 | push slot << 16,
-  //                     b = x index, c = y index (L* kinds)
-  // linked (interpret): a = kind | y-is-vector << 8, b = x byte offset,
-  //                     c = y byte offset (L*) or push-slot byte offset (PUSHLOAD),
+  //                     b = x index, c = y index (L*/P* kinds)
+  // linked (interpret): a = kind | y-is-vector << 8 | push slot << 16,
+  //                     b = x byte offset, c = y byte offset (L*/P*),
   //                     d = x lane mask (~0 vector row, 0 broadcast constant);
   //                     feature offsets carry kFeatGlobal when features stay in HBM,
   //                     constants kConstGlobal in the lean (huge-program) configuration

@@ -156,13 +156,13 @@ __global__ void k_compile(const uint8_t* __restrict__ tags, const int32_t* __res
       const int32_t op = C[n];
       if (st == 0) {
         if (la && lb) {
-          if (pending >= 0) {                 // PUSHLOAD l ; acc = acc OP r
-            emit_leaf(K_LOAD, l);
-            emit_leaf(fwd(op), r);
+          uint32_t xc, xi, yc, yi;
+          leaf(l, xc, xi);
+          leaf(r, yc, yi);
+          if (pending >= 0) {                 // spill, then acc = l OP r
+            out[pc++] = abstract_ins(K_PADD + (uint32_t)op, xc, xi, (uint32_t)pending, yc, yi);
+            pending = -1;
           } else {                            // acc = l OP r
-            uint32_t xc, xi, yc, yi;
-            leaf(l, xc, xi);
-            leaf(r, yc, yi);
             out[pc++] = abstract_ins(K_LADD + (uint32_t)op, xc, xi, 0, yc, yi);
           }
           --top;
@@ -259,9 +259,8 @@ __global__ void k_link(const Ins* __restrict__ code, Ins* __restrict__ exe, cons
     Ins o;
     o.b = off(xcls, in.b, xvec);
     o.d = xvec ? 0xffffffffu : 0u;
-    if (kind >= K_LADD) o.c = off(ycls, in.c, yvec);
-    else o.c = (frows + push) * rowb;
-    o.a = kind | (yvec << 8);
+    o.c = kind >= K_LADD ? off(ycls, in.c, yvec) : 0u;
+    o.a = kind | (yvec << 8) | (push << 16);
     exe[g * k1 + i] = o;
   }
 }
@@ -284,7 +283,8 @@ __device__ __forceinline__ uint4 lds_u128(uint32_t p) {
 
 template <int NT, int CPT, int MODE, typename TOut, bool kXSmem, bool kLean>
 __global__ void __launch_bounds__(NT) k_interpret(InterpArgs a, int64_t gpb,
-                                                  uint32_t crow_off, uint32_t prog_off) {
+                                                  uint32_t stack_off, uint32_t crow_off,
+                                                  uint32_t prog_off) {
   constexpr int TILE = NT * CPT;
   constexpr uint32_t CSTRIDE = NT * 8;          // bytes between a thread's cases
   extern __shared__ __align__(16) unsigned char smem[];
@@ -318,6 +318,7 @@ __global__ void __launch_bounds__(NT) k_interpret(InterpArgs a, int64_t gpb,
   uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
   asm volatile("" : "+r"(sbase));              // keep it in a register (no per-iteration remat)
   const uint32_t pbase = sbase + prog_off;
+  const uint32_t sp0 = sbase + stack_off + tid8;   // this thread's spill slot 0, case 0
   const int64_t cstride = a.k1 - 1;
   unsigned long long nonfinite = 0;
 
@@ -380,7 +381,7 @@ __global__ void __launch_bounds__(NT) k_interpret(InterpArgs a, int64_t gpb,
       if (kind >= K_LADD) fetch(in.z, (in.x & 0x100) ? 0xffffffffu : 0u, y);   // second leaf
       // one warp-uniform jump (interp_dispatch.inc); each arm is straight-line
       // code over the CPT cases of this thread, one IEEE rounding per case
-      Dispatch<CPT, CSTRIDE>::run(acc, x, y, kind, sbase + in.z + tid8, a.eps);
+      Dispatch<CPT, CSTRIDE>::run(acc, x, y, kind, in.x, sp0, a.eps);
     }
     // ---- epilogue: non-finite -> 0.0 counted (core.py:348-356), then store
     double sse_tr = 0.0, sse_te = 0.0;
@@ -453,7 +454,7 @@ void launch_cfg(const InterpArgs& a, cudaStream_t s) {
   dim3 grid((unsigned)ntiles, (unsigned)gy);
   auto k = k_interpret<NT, CPT, MODE, TOut, kXSmem, kLean>;
   GSGP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k<<<grid, NT, smem, s>>>(a, gpb, (frows + (uint32_t)a.maxdepth) * rowb,
+  k<<<grid, NT, smem, s>>>(a, gpb, frows * rowb, (frows + (uint32_t)a.maxdepth) * rowb,
                            (uint32_t)cfg_rows_bytes(c, a));
   GSGP_CUDA(cudaGetLastError());
 }
