@@ -319,6 +319,10 @@ __global__ void __launch_bounds__(NT) k_interpret(InterpArgs a, int64_t gpb,
   asm volatile("" : "+r"(sbase));              // keep it in a register (no per-iteration remat)
   const uint32_t pbase = sbase + prog_off;
   const uint32_t sp0 = sbase + stack_off + tid8;   // this thread's spill slot 0, case 0
+  // division fast path: denominators need |hi word| >= max(2^-500, hi(eps) + 1),
+  // compared as f32 bit patterns (interp_dispatch.inc)
+  const float dlo = __uint_as_float(max(523u << 20,
+      (uint32_t)(__double_as_longlong(fabs(a.eps)) >> 32) + 1u));
   const int64_t cstride = a.k1 - 1;
   unsigned long long nonfinite = 0;
 
@@ -381,7 +385,7 @@ __global__ void __launch_bounds__(NT) k_interpret(InterpArgs a, int64_t gpb,
       if (kind >= K_LADD) fetch(in.z, (in.x & 0x100) ? 0xffffffffu : 0u, y);   // second leaf
       // one warp-uniform jump (interp_dispatch.inc); each arm is straight-line
       // code over the CPT cases of this thread, one IEEE rounding per case
-      Dispatch<CPT, CSTRIDE>::run(acc, x, y, kind, in.x, sp0, a.eps);
+      Dispatch<CPT, CSTRIDE>::run(acc, x, y, kind, in.x, sp0, a.eps, dlo);
     }
     // ---- epilogue: non-finite -> 0.0 counted (core.py:348-356), then store
     double sse_tr = 0.0, sse_te = 0.0;
