@@ -402,9 +402,10 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
     ip.y = nullptr;
 
     const size_t row_bytes = (size_t)l * 8 + 8;             // features + target of one case
-    int64_t chunk = (int64_t)(kUploadChunkBytes / row_bytes) / 1024 * 1024;
-    if (const char* e = getenv("GSGP_UPLOAD_CHUNK")) chunk = atoll(e) / 1024 * 1024;   // tests
-    if (chunk < 1024) chunk = 1024;                          // multiple of every interpreter tile
+    // chunks are multiples of 3072 = lcm of every interpreter tile (128 .. 1024, 384)
+    int64_t chunk = (int64_t)(kUploadChunkBytes / row_bytes) / 3072 * 3072;
+    if (const char* e = getenv("GSGP_UPLOAD_CHUNK")) chunk = atoll(e) / 3072 * 3072;   // tests
+    if (chunk < 3072) chunk = 3072;
     if (chunk > N) chunk = (N + itile - 1) / itile * itile;
     const int64_t nchunks = (N + chunk - 1) / chunk;
     PinnedStage& pin = pinned_stage(2 * (size_t)chunk * row_bytes);

@@ -205,7 +205,7 @@ struct InterpCfg {
                 // shared memory, so any program size fits (huge k fallback)
 };
 constexpr InterpCfg kCfgs[] = {{128, 4, true, false}, {64, 8, true, false}, {128, 4, false, false},
-                               {128, 2, true, false}, {128, 1, false, true}};
+                               {128, 2, true, false}, {128, 1, false, true}, {128, 3, true, false}};
 constexpr int kNumCfgs = sizeof(kCfgs) / sizeof(kCfgs[0]);
 constexpr size_t kSmemCap = 200 * 1024;
 
@@ -225,7 +225,10 @@ int choose_cfg(const InterpArgs& a) {
   const char* env = getenv("GSGP_INTERP_CFG");   // experiments / tests (read per launch)
   const int forced = env ? atoi(env) : -1;
   if (forced >= 0 && forced < kNumCfgs && cfg_smem(kCfgs[forced], a) <= kSmemCap) return forced;
-  // features in shared memory while the tile keeps >= 3 blocks per SM
+  // features in shared memory while the tile keeps >= 3 blocks per SM; the
+  // 384-case tile (128 x 3) fits 5 blocks (20 warps) where 128 x 4 fits 4:
+  // measured 1-4 % faster (profiles/r01/README.md)
+  if (cfg_smem(kCfgs[5], a) <= 45 * 1024) return 5;
   if (cfg_smem(kCfgs[0], a) <= 72 * 1024) return 0;
   if (cfg_smem(kCfgs[2], a) <= 72 * 1024) return 2;
   if (cfg_smem(kCfgs[2], a) <= kSmemCap) return 2;
@@ -470,6 +473,7 @@ void launch_mode(const InterpArgs& a, cudaStream_t s) {
     case 1: launch_cfg<64, 8, MODE, TOut, true>(a, s); break;
     case 2: launch_cfg<128, 4, MODE, TOut, false>(a, s); break;
     case 3: launch_cfg<128, 2, MODE, TOut, true>(a, s); break;
+    case 5: launch_cfg<128, 3, MODE, TOut, true>(a, s); break;
     default: launch_cfg<128, 1, MODE, TOut, false, true>(a, s); break;
   }
 }

@@ -52,7 +52,7 @@ def _elite(res):
 def test_random_run_matches_engine_restatement(seed, monkeypatch):
     kw, Xtr, ytr, Xte, yte = _random_case(seed)
     if seed % 4 == 1:
-        monkeypatch.setenv("GSGP_UPLOAD_CHUNK", "1024")
+        monkeypatch.setenv("GSGP_UPLOAD_CHUNK", "3072")
     res = G.run_evolution(G.RunConfig(**kw), G.Dataset(Xtr, ytr), G.Dataset(Xte, yte),
                           virtual_shards=1 + seed % 3)
     o = engine32.run32(R.Cfg(**kw), Xtr, ytr, Xte, yte)
