@@ -355,3 +355,49 @@ def test_interpreter_lean_configuration_matches(monkeypatch):
     b = G.compute_semantics(pop, X, RunConfig(program_size=k))
     assert np.array_equal(a.view(np.uint64), ref.view(np.uint64))
     assert np.array_equal(b.view(np.uint64), ref.view(np.uint64))
+
+
+def _hard_division_operands(rng, n):
+    """In-range (|v| in [2^-499, 2^499]) operands dominated by near-halfway
+    quotients: mantissas 1 - j*2^-53 and 1 + j*2^-52 for small j, powers of
+    two, and random mantissas, with random exponents and signs."""
+    kind = rng.integers(0, 4, n)
+    j = rng.integers(1, 64, n).astype(np.float64)
+    mant = np.where(kind == 0, 1.0 - j * 2.0 ** -53,
+                    np.where(kind == 1, 1.0 + j * 2.0 ** -52,
+                             np.where(kind == 2, 1.0, rng.uniform(1, 2, n))))
+    v = mant * np.exp2(rng.integers(-499, 499, n).astype(np.float64))
+    return np.where(rng.random(n) < 0.5, -v, v)
+
+
+def test_interpreter_division_fast_path_near_halfway_quotients():
+    """Every case of every group inside the fast-path range, so whole groups
+    take the Newton path: x0/x1, x1/x0 and 1/x for near-halfway operands
+    (1/nextafter(2^501, 0) misrounded with a zero-low-word reciprocal seed)
+    must be bit-exact with numpy's IEEE division, for every tile config."""
+    rng = np.random.default_rng(21)
+    n = 300_000
+    X = np.stack([_hard_division_operands(rng, n), _hard_division_operands(rng, n)], axis=1)
+    F, V, DIV = int(GeneTag.FUNCTION), int(GeneTag.FEATURE), int(FunctionOp.DIV)
+    progs = [[(V, 0), (V, 1), (F, DIV)],
+             [(V, 1), (V, 0), (F, DIV)],
+             [(V, 0), (V, 0), (F, DIV), (V, 1), (F, DIV)],            # 1 / x1 (x0/x0 == 1)
+             [(V, 1), (V, 1), (F, DIV), (V, 0), (F, DIV), (V, 1), (F, DIV)]]
+    k = max(len(p) for p in progs)
+    tags = np.full((len(progs), k), int(GeneTag.CONSTANT), np.uint8)
+    codes = np.zeros((len(progs), k), np.int32)
+    consts = np.full((len(progs), k), 2.5)
+    for i, p in enumerate(progs):
+        off = k - len(p)
+        for jj, (t, c) in enumerate(p):
+            tags[i, off + jj], codes[i, off + jj] = t, c
+    ref, _ = R.semantics(tags, codes, consts, X, 1e-6)
+    pop = Population(tags, codes, consts)
+    import os
+    for cfg in ("0", "1", "2", "3", "4", "5"):
+        os.environ["GSGP_INTERP_CFG"] = cfg
+        try:
+            S = G.compute_semantics(pop, X, RunConfig(program_size=k))
+        finally:
+            del os.environ["GSGP_INTERP_CFG"]
+        assert np.array_equal(S.view(np.uint64), ref.view(np.uint64)), cfg
