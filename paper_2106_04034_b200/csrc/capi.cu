@@ -19,6 +19,7 @@ void run_engine(const gsgp_config*, const double*, const double*, int64_t, const
 void comm_unique_id(unsigned char*);
 void comm_init(int, int, const unsigned char*);
 void comm_destroy();
+void trim_device_memory();
 void shard_range(int64_t, int64_t, int64_t, int64_t*, int64_t*);
 
 namespace {
@@ -126,12 +127,8 @@ int gsgp_set_device(int device) {
 int gsgp_trim_device_memory(void) {
   return guarded([&] {
     require_device();
-    int dev = 0;
-    GSGP_CUDA(cudaGetDevice(&dev));
-    cudaMemPool_t pool;
-    GSGP_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
     GSGP_CUDA(cudaDeviceSynchronize());
-    GSGP_CUDA(cudaMemPoolTrimTo(pool, 0));
+    trim_device_memory();
   });
 }
 

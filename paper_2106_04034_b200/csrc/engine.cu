@@ -15,6 +15,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <vector>
 
 #include "gsgp_b200.h"
@@ -23,48 +24,83 @@
 namespace gsgp {
 
 // ------------------------------------------------------------- device memory
-// Engine buffers come from the device's stream-ordered memory pool on the
-// engine stream (cudaMallocAsync / cudaFreeAsync).  The pool keeps its memory
-// between runs (release threshold = max), so a job's second run allocates
-// and frees its ~100 GB working set without driver calls — a plain cudaFree
-// of a 51 GB buffer was measured at up to 1.6 s.  gsgp_trim_device_memory()
-// hands the pool's memory back.
-thread_local cudaStream_t g_alloc_stream = nullptr;
+// Engine buffers come from a small process-level cache of device blocks:
+// a run's release parks its blocks (after its stream has drained) and the
+// next run reuses them, so a job's second run neither allocates nor frees
+// its ~100 GB working set (a plain cudaFree of a 51 GB buffer was measured
+// at up to 1.6 s; growing the stream-ordered pool at up to 4.8 s).  First
+// allocations are plain cudaMalloc; an allocation failure empties the cache
+// and retries.  gsgp_trim_device_memory() frees the cache.
+struct CachedBlock {
+  void* p;
+  size_t bytes;
+};
+std::mutex g_cache_mu;
+std::vector<CachedBlock> g_cache;
 
-void configure_pool_once() {
-  static bool done = false;
-  if (done) return;
-  int dev = 0;
-  GSGP_CUDA(cudaGetDevice(&dev));
-  cudaMemPool_t pool;
-  GSGP_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
-  uint64_t keep = UINT64_MAX;
-  GSGP_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
-  done = true;
+void cache_trim() {
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  for (auto& b : g_cache) cudaFree(b.p);
+  g_cache.clear();
 }
+
+void* cache_alloc(size_t bytes, size_t* got) {
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    int best = -1;
+    for (int i = 0; i < (int)g_cache.size(); ++i)     // smallest block within 1.25x
+      if (g_cache[i].bytes >= bytes && g_cache[i].bytes <= bytes + bytes / 4 &&
+          (best < 0 || g_cache[i].bytes < g_cache[best].bytes))
+        best = i;
+    if (best >= 0) {
+      CachedBlock b = g_cache[best];
+      g_cache.erase(g_cache.begin() + best);
+      *got = b.bytes;
+      return b.p;
+    }
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    cache_trim();
+    e = cudaMalloc(&p, bytes);
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw Error{e == cudaErrorMemoryAllocation ? ERR_OOM : ERR_CUDA,
+                "cudaMalloc(" + std::to_string(bytes) + " bytes): " + cudaGetErrorString(e)};
+  }
+  *got = bytes;
+  return p;
+}
+
+thread_local cudaStream_t g_alloc_stream = nullptr;   // stream a released block may still be used on
 
 struct DevBuf {
   void* p = nullptr;
+  size_t bytes = 0;
   cudaStream_t s = nullptr;
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
   ~DevBuf() { release(); }
   void release() {
-    if (p) cudaFreeAsync(p, s);
+    if (!p) return;
+    // the block is parked for reuse by any stream: drain its stream first
+    if (cudaStreamSynchronize(s) == cudaSuccess) {
+      std::lock_guard<std::mutex> lk(g_cache_mu);
+      g_cache.push_back({p, bytes});
+    } else {
+      cudaGetLastError();
+      cudaFree(p);
+    }
     p = nullptr;
   }
-  void alloc(size_t bytes) {
+  void alloc(size_t n) {
     release();
-    if (bytes == 0) bytes = 16;
     s = g_alloc_stream;
-    cudaError_t e = cudaMallocAsync(&p, bytes, s);
-    if (e != cudaSuccess) {
-      p = nullptr;
-      cudaGetLastError();
-      throw Error{e == cudaErrorMemoryAllocation ? ERR_OOM : ERR_CUDA,
-                  "cudaMallocAsync(" + std::to_string(bytes) + " bytes): " + cudaGetErrorString(e)};
-    }
+    p = cache_alloc(n == 0 ? 16 : n, &bytes);
   }
   template <typename T> T* as() const { return reinterpret_cast<T*>(p); }
 };
@@ -147,6 +183,8 @@ void comm_init(int world, int rank, const unsigned char* id) {
   std::memcpy(u.internal, id, NCCL_UNIQUE_ID_BYTES);
   nccl().check(nccl().commInitRank(&c.comm, world, u, rank), "ncclCommInitRank");
 }
+
+void trim_device_memory() { cache_trim(); }
 
 void comm_destroy() {
   CommState& c = comm_state();
@@ -247,8 +285,7 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   } sg{st};
   GSGP_CUDA(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
   StreamGuard sg_up{up};
-  configure_pool_once();
-  struct AllocStream {            // DevBufs of this run allocate/free on st
+  struct AllocStream {            // DevBufs of this run drain st before parking their blocks
     cudaStream_t prev;
     explicit AllocStream(cudaStream_t s) : prev(g_alloc_stream) { g_alloc_stream = s; }
     ~AllocStream() { g_alloc_stream = prev; }
@@ -414,9 +451,7 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
       Xr[b].alloc(chunk * l * 8);
       XT[b].alloc(chunk * l * 8);
     }
-    Event ev_h2d[2], ev_done[2], e_start, e_first, ev_alloc;
-    GSGP_CUDA(cudaEventRecord(ev_alloc.e, st));        // pool allocations are ordered on st
-    GSGP_CUDA(cudaStreamWaitEvent(up, ev_alloc.e, 0));
+    Event ev_h2d[2], ev_done[2], e_start, e_first;
     std::vector<std::unique_ptr<Event>> ev_k;
     GSGP_CUDA(cudaEventRecord(e_start.e, st));
     for (int64_t c = 0; c < nchunks; ++c) {

@@ -79,8 +79,8 @@ def uniform_array(seed: int, stream: int, counters: np.ndarray) -> np.ndarray:
 
 
 def release_device_memory() -> None:
-    """Hand the engine's cached device memory back to the driver (runs keep
-    their working set in a stream-ordered pool for the next run)."""
+    """Hand the engine's cached device memory back to the driver (a run parks
+    its device blocks for the next run instead of freeing them)."""
     check(_lib.load().gsgp_trim_device_memory())
 
 
