@@ -237,6 +237,9 @@ struct PinnedStage {
 };
 PinnedStage& pinned_stage(size_t bytes) {
   static PinnedStage s;
+  // allocate the full double buffer on first use (page-locking ~100 MB costs
+  // ~50 ms; growing it run by run would charge that to later runs)
+  if (bytes < 2 * kUploadChunkBytes + (64u << 10)) bytes = 2 * kUploadChunkBytes + (64u << 10);
   if (s.bytes < bytes) {
     if (s.p) GSGP_CUDA(cudaFreeHost(s.p));
     s.p = nullptr;

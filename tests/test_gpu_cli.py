@@ -78,3 +78,20 @@ def test_timed_run_and_sweep_on_device():
     assert stages[:4] == ["create_population", "compute_semantics", "generation", "total"]
     assert stages[-1] == "error"
     assert all(r["millis"] >= 0 for r in rows[:4])
+
+
+def test_bench_cli_program_size_sweep(tmp_path):
+    """gsgp-bench (gsgp/harness.py:130-152) on the device: one CSV row per
+    stage and cell in the reference schema; ComputeSemantics time grows with
+    program size (the paper's k sensitivity, pkg/tests/test_harness.py:62-68)."""
+    import csv
+
+    from paper_2106_04034_b200.harness import main
+    out = tmp_path / "sweep.csv"
+    assert main(["--m", "256", "--n", "400000", "--k", "127,1023,2047", "--out", str(out)]) == 0
+    with open(out, newline="") as fh:
+        rows = list(csv.DictReader(fh))
+    assert len(rows) == 12 and {r["stage"] for r in rows} == {
+        "create_population", "compute_semantics", "generation", "total"}
+    sem = [float(r["millis"]) for r in rows if r["stage"] == "compute_semantics"]
+    assert sem[0] < sem[1] < sem[2]
