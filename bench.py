@@ -155,9 +155,16 @@ def run_ours(args):
     import paper_2106_04034_b200 as G
     from paper_2106_04034_b200 import _lib, dist
     lib = _lib.load()
-    _lib.check(lib.gsgp_set_device(local))
+    # GSGP_BENCH_HOST_EXCHANGE=1: harness check of the N>1 path with every
+    # rank on GPU 0 and the collectives over host memory + gloo (no NCCL);
+    # its numbers are not bench values
+    host_xchg = world > 1 and os.environ.get("GSGP_BENCH_HOST_EXCHANGE") == "1"
+    _lib.check(lib.gsgp_set_device(0 if host_xchg else local))
     if world > 1:
-        dist.init_from_torch()
+        if host_xchg:
+            dist.init_host_exchange()
+        else:
+            dist.init_from_torch()
 
     def barrier():
         if td:

@@ -152,6 +152,12 @@ int gsgp_run(const gsgp_config* cfg, const double* Xtr, const double* ytr, int64
  * allreduces the per-row partial SSE each generation (NCCL over NVLink). */
 int gsgp_comm_unique_id(unsigned char id[128]);
 int gsgp_comm_init(int world, int rank, const unsigned char id[128]);
+/* Test transport for the same collectives: `allreduce` sums a HOST buffer
+   of `count` elements (dtype 0 fp64, 1 int32, 2 uint64) over the ranks in
+   place (e.g. torch.distributed over gloo), so the multi-rank engine path
+   runs with several processes sharing one GPU.  Runs use direct launches
+   (no graph) in this mode. */
+int gsgp_comm_init_host(int world, int rank, void (*allreduce)(void* buf, int64_t count, int32_t dtype));
 int gsgp_comm_destroy(void);
 /* contiguous case slice [lo, hi) of shard `index` out of `count` */
 void gsgp_shard_range(int64_t n, int64_t count, int64_t index, int64_t* lo, int64_t* hi);

@@ -28,7 +28,8 @@ EXPORTS = (
     "gsgp_version", "gsgp_last_error", "gsgp_device_info", "gsgp_set_device", "gsgp_trim_device_memory", "gsgp_rng_draw",
     "gsgp_derive_seed", "gsgp_create_population", "gsgp_compute_semantics", "gsgp_compute_fitness",
     "gsgp_build_mutation_plan", "gsgp_gsm", "gsgp_gsm_step_f32", "gsgp_survive", "gsgp_run",
-    "gsgp_comm_unique_id", "gsgp_comm_init", "gsgp_comm_destroy", "gsgp_shard_range",
+    "gsgp_comm_unique_id", "gsgp_comm_init", "gsgp_comm_init_host", "gsgp_comm_destroy",
+    "gsgp_shard_range",
     "gsgp_sigmoid", "gsgp_argminmax",
 )
 
@@ -86,6 +87,7 @@ _SIGS = {
     "gsgp_run": (C.c_int, [C.POINTER(GsgpConfig), P, P, I64, P, P, I64, I32, C.POINTER(GsgpOutputs)]),
     "gsgp_comm_unique_id": (C.c_int, [P]),
     "gsgp_comm_init": (C.c_int, [C.c_int, C.c_int, P]),
+    "gsgp_comm_init_host": (C.c_int, [C.c_int, C.c_int, P]),
     "gsgp_comm_destroy": (C.c_int, []),
     "gsgp_shard_range": (None, [I64, I64, I64, P, P]),
     "gsgp_sigmoid": (C.c_int, [P, I64, P]),

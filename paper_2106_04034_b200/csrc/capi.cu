@@ -19,6 +19,7 @@ void run_engine(const gsgp_config*, const double*, const double*, int64_t, const
 void comm_unique_id(unsigned char*);
 void comm_init(int, int, const unsigned char*);
 void comm_destroy();
+void comm_init_host(int world, int rank, void (*fn)(void*, int64_t, int32_t));
 void trim_device_memory();
 void shard_range(int64_t, int64_t, int64_t, int64_t*, int64_t*);
 
@@ -434,6 +435,10 @@ int gsgp_comm_init(int world, int rank, const unsigned char id[128]) {
     require_device();
     comm_init(world, rank, id);
   });
+}
+
+int gsgp_comm_init_host(int world, int rank, void (*allreduce)(void* buf, int64_t count, int32_t dtype)) {
+  return guarded([&] { comm_init_host(world, rank, allreduce); });
 }
 
 int gsgp_comm_destroy(void) {

@@ -152,8 +152,15 @@ NcclApi& nccl() {
   return api;
 }
 
+// Host exchange (tests): the same collectives through a host callback that
+// sums a host buffer over the ranks (e.g. torch.distributed over gloo), so
+// the multi-rank engine path runs with several processes on one GPU.  dtype:
+// 0 fp64, 1 int32, 2 uint64.  Not graph-capturable: runs use direct launches.
+typedef void (*HostAllreduce)(void* buf, int64_t count, int32_t dtype);
+
 struct CommState {
   ncclComm_t comm = nullptr;
+  HostAllreduce host = nullptr;
   int world = 1, rank = 0;
 };
 CommState& comm_state() {
@@ -186,10 +193,41 @@ void comm_init(int world, int rank, const unsigned char* id) {
 
 void trim_device_memory() { cache_trim(); }
 
+void comm_init_host(int world, int rank, HostAllreduce fn) {
+  GSGP_REQUIRE(world >= 1 && rank >= 0 && rank < world && fn, "bad world/rank/callback");
+  CommState& c = comm_state();
+  if (c.comm) {
+    nccl().commDestroy(c.comm);
+    c.comm = nullptr;
+  }
+  c.world = world;
+  c.rank = rank;
+  c.host = fn;
+}
+
+// in-place sum over the ranks of a device buffer on stream s (NCCL or host)
+void allreduce_sum(void* dev, int64_t count, int32_t dtype, cudaStream_t s, const char* what) {
+  CommState& c = comm_state();
+  if (c.world <= 1) return;
+  if (c.host) {
+    const size_t esz = dtype == 1 ? 4 : 8;
+    std::vector<unsigned char> h(count * esz);
+    GSGP_CUDA(cudaMemcpyAsync(h.data(), dev, count * esz, cudaMemcpyDeviceToHost, s));
+    GSGP_CUDA(cudaStreamSynchronize(s));
+    c.host(h.data(), count, dtype);
+    GSGP_CUDA(cudaMemcpyAsync(dev, h.data(), count * esz, cudaMemcpyHostToDevice, s));
+    GSGP_CUDA(cudaStreamSynchronize(s));
+    return;
+  }
+  const ncclDataType_t t = dtype == 0 ? ncclFloat64 : (dtype == 1 ? ncclInt32 : ncclUint64);
+  nccl().check(nccl().allReduce(dev, dev, count, t, ncclSum, c.comm, s), what);
+}
+
 void comm_destroy() {
   CommState& c = comm_state();
   if (c.comm) nccl().commDestroy(c.comm);
   c.comm = nullptr;
+  c.host = nullptr;
   c.world = 1;
   c.rank = 0;
 }
@@ -542,9 +580,7 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
       for (auto& p : sh) v.push_back((p.get()->*mem).as<double>());
       launch_sum_shards(v.data(), G, m * 2, dst, s);
     }
-    if (W > 1)
-      nccl().check(nccl().allReduce(dst, dst, m * 2, ncclFloat64, ncclSum, cs.comm, s),
-                   "ncclAllReduce(sse)");
+    if (W > 1) allreduce_sum(dst, m * 2, 0, s, "ncclAllReduce(sse)");
   };
   auto exchange = [&](cudaStream_t s) { exchange_of(&Shard::sse, sse_vec, s); };
   exchange(st);
@@ -553,10 +589,9 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
     DevBuf bits;
     bits.alloc(m * 2 * 4);
     k_wide_split<<<nblk(m), 256, 0, st>>>(wide.as<int32_t>(), m, bits.as<int32_t>());
-    nccl().check(nccl().allReduce(bits.p, bits.p, m * 2, ncclInt32, ncclSum, cs.comm, st), "ncclAllReduce(wide)");
+    allreduce_sum(bits.p, m * 2, 1, st, "ncclAllReduce(wide)");
     k_wide_merge<<<nblk(m), 256, 0, st>>>(bits.as<int32_t>(), m, wide.as<int32_t>());
-    nccl().check(nccl().allReduce(nonfinite.p, nonfinite.p, 1, ncclUint64, ncclSum, cs.comm, st),
-                 "ncclAllReduce(overflow)");
+    allreduce_sum(nonfinite.p, 1, 2, st, "ncclAllReduce(overflow)");
     GSGP_CUDA(cudaStreamSynchronize(st));
   }
 
@@ -647,7 +682,7 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   if (g > 0) {
     cudaGraphExec_t exec = nullptr;
     cudaGraph_t graph = nullptr;
-    if (!timed && cfg->use_graph) {
+    if (!timed && cfg->use_graph && !(W > 1 && cs.host)) {
       GSGP_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
       enqueue_generation(st, nullptr, nullptr);
       GSGP_CUDA(cudaStreamEndCapture(st, &graph));

@@ -41,6 +41,34 @@ def init_from_torch(group=None) -> tuple[int, int]:
     return world, rank
 
 
+HOST_ALLREDUCE = C.CFUNCTYPE(None, C.c_void_p, C.c_int64, C.c_int32)
+_host_cb = None   # keep the ctypes callback alive while the library holds it
+
+
+def init_host_exchange(group=None) -> tuple[int, int]:
+    """Test transport: the engine's collectives go through host memory and
+    torch.distributed (e.g. gloo) instead of NCCL, so several ranks can share
+    one GPU (`gsgp_comm_init_host`).  Same partitioning and exchanged values
+    as the NCCL path; runs use direct launches instead of a CUDA graph."""
+    import torch
+    import torch.distributed as td
+    global _host_cb
+    world, rank = td.get_world_size(group), td.get_rank(group)
+    dtypes = {0: (np.float64, 8), 1: (np.int32, 4), 2: (np.uint64, 8)}
+
+    def allreduce(ptr, count, dtype):
+        npt, esz = dtypes[int(dtype)]
+        buf = np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_ubyte)), shape=(count * esz,))
+        arr = buf.view(npt)
+        t = torch.from_numpy(arr.astype(np.int64) if npt is np.uint64 else arr.copy())
+        td.all_reduce(t, op=td.ReduceOp.SUM, group=group)
+        arr[:] = t.numpy().astype(npt)
+
+    _host_cb = HOST_ALLREDUCE(allreduce)
+    check(_lib.load().gsgp_comm_init_host(world, rank, C.cast(_host_cb, C.c_void_p)))
+    return world, rank
+
+
 def destroy() -> None:
     check(_lib.load().gsgp_comm_destroy())
 

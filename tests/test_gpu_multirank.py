@@ -1,0 +1,79 @@
+"""The engine's multi-rank path (case sharding + per-generation exchange,
+SURVEY §8e) with 2 and 3 real processes sharing this GPU: the collectives
+go through `dist.init_host_exchange` (host memory + gloo) instead of NCCL —
+same partition, same exchanged values, same decision logic in the library.
+Every rank must return the single-process run's elite trace and traces
+(bit-identical: the exchanged SSE partial sums only change the summation
+grouping) and the reference's golden elite trace; the gathered elite
+semantics must equal the single-process elite semantics."""
+
+from __future__ import annotations
+
+import ast
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as td
+import torch.multiprocessing as mp
+
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, name, vshards, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    td.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2106_04034_b200 as G
+        from paper_2106_04034_b200 import dist
+        dist.init_host_exchange()
+        g = golden(name)
+        cfg = G.RunConfig(**ast.literal_eval(str(g["cfg"][0])))
+        res = G.run_evolution(cfg, G.Dataset(g["Xtr"], g["ytr"]), G.Dataset(g["Xte"], g["yte"]),
+                              virtual_shards=vshards)
+        full = dist.gather_elite_semantics(res, g["Xtr"].shape[0])
+        elite = [(e.elite.source, e.elite.index, e.elite.slot) for e in res.lineage.entries]
+        q.put((rank, elite, res.train_fitness.tolist(), res.test_fitness.tolist(),
+               res.overflow_replacements, full.tolist()))
+        dist.destroy()
+    finally:
+        td.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,world,vshards", [("accept", 2, 1), ("c1", 3, 1), ("c2s", 2, 2)])
+def test_ranks_sharing_a_gpu_reproduce_single_process_run(name, world, vshards):
+    import paper_2106_04034_b200 as G
+    g = golden(name)
+    cfg = G.RunConfig(**ast.literal_eval(str(g["cfg"][0])))
+    one = G.run_evolution(cfg, G.Dataset(g["Xtr"], g["ytr"]), G.Dataset(g["Xte"], g["yte"]))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, name, vshards, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = sorted(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    ref_elite = [(("parent" if s == 0 else "offspring"), int(i), int(w))
+                 for s, i, w in zip(g["src"], g["idx"], g["slot"])]
+    one_elite = [(e.elite.source, e.elite.index, e.elite.slot) for e in one.lineage.entries]
+    assert one_elite == ref_elite
+    for rank, elite, train, test, overflow, full in got:
+        assert elite == one_elite, rank
+        np.testing.assert_allclose(train, one.train_fitness, rtol=1e-12, atol=0)
+        np.testing.assert_allclose(test, one.test_fitness, rtol=1e-12, atol=0)
+        assert overflow == one.overflow_replacements
+        assert np.array_equal(np.array(full), one.elite_train_semantics)
+    assert all(r[2] == got[0][2] and r[3] == got[0][3] for r in got)   # identical on every rank
