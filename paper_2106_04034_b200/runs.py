@@ -57,9 +57,10 @@ def _world(group):
 
 
 def select_local_device() -> None:
-    """Bind this process to its GPU (LOCAL_RANK) before its first run."""
+    """Bind this process to its GPU (LOCAL_RANK) before its first run
+    (GSGP_SHARED_GPU=1: every rank on GPU 0, for tests on a one-GPU box)."""
     from . import _lib
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = 0 if os.environ.get("GSGP_SHARED_GPU") == "1" else int(os.environ.get("LOCAL_RANK", "0"))
     _lib.check(_lib.load().gsgp_set_device(local))
 
 

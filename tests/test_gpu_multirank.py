@@ -77,3 +77,50 @@ def test_ranks_sharing_a_gpu_reproduce_single_process_run(name, world, vshards):
         assert overflow == one.overflow_replacements
         assert np.array_equal(np.array(full), one.elite_train_semantics)
     assert all(r[2] == got[0][2] and r[3] == got[0][3] for r in got)   # identical on every rank
+
+
+def _replica_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ["GSGP_SHARED_GPU"] = "1"
+    td.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import dataclasses
+
+        import paper_2106_04034_b200 as G
+        from paper_2106_04034_b200.runs import select_local_device
+        select_local_device()
+        g = golden("c1")
+        cfg = dataclasses.replace(G.RunConfig(**ast.literal_eval(str(g["cfg"][0]))), runs=5,
+                                  generations=12)
+        ran = []
+        out = G.run_many(cfg, G.Dataset(g["Xtr"], g["ytr"]), G.Dataset(g["Xte"], g["yte"]),
+                         on_result=lambda i, r: ran.append(i))
+        q.put((rank, ran, [None if o is None else o.train_fitness.tolist() for o in out]))
+    finally:
+        td.destroy_process_group()
+
+
+def test_replica_runs_across_ranks_match_sequential_runs():
+    """run_many with 2 real ranks on this GPU: run i on
+    rank i % 2, full results gathered to rank 0 in run order, equal to the
+    runs executed one by one in this process."""
+    import dataclasses
+
+    import paper_2106_04034_b200 as G
+    g = golden("c1")
+    cfg = dataclasses.replace(G.RunConfig(**ast.literal_eval(str(g["cfg"][0]))), runs=5, generations=12)
+    tr, te = G.Dataset(g["Xtr"], g["ytr"]), G.Dataset(g["Xte"], g["yte"])
+    seq = [G.run_evolution(cfg.with_seed(s), tr, te).train_fitness.tolist() for s in G.run_seeds(cfg)]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_replica_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = sorted(q.get(timeout=600) for _ in range(2))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert got[0][1] == [0, 2, 4] and got[1][1] == [1, 3]
+    assert got[0][2] == seq
