@@ -131,6 +131,23 @@ def bytes_per_generation(plans, N: int, m: int) -> np.ndarray:
     return np.array(out)
 
 
+def interp_line(res, c, world: int) -> dict:
+    """ComputeSemantics: issue/fp64 bound, reported as function-
+    node evaluations per second (one compiled instruction = one function node
+    of the dead-code-eliminated, constant-folded tree) with its compulsory
+    bytes (features read once, fp32 semantics written)."""
+    N = (c["ntr"] + c["nte"]) / world
+    ins = res.device["program_instructions"]
+    ms = res.device["init_ms"]
+    t = (ms["interpret_population"] + ms["interpret_pool"]) / 1e3
+    evals = (ins["population"] + ins["pool"]) * N
+    byts = N * c["l"] * 8 + (c["m"] + c["r"]) * N * 4
+    return {"node_evals_per_s": evals / t if t > 0 else None, "unit": "function-node evals/s",
+            "seconds": t, "mean_program_instructions": (ins["population"] + ins["pool"]) / (c["m"] + c["r"]),
+            "compulsory_bytes": byts, "compulsory_GBps": byts / t / 1e9 if t > 0 else None,
+            "bound": "issue/fp64 latency (see DESIGN.md §6)"}
+
+
 def cpu_leg(c, budget_s: float):
     from oracle import cpu_bench
     t = cpu_bench.time_loop(c["m"], c["r"], c["ntr"], c["nte"], budget_s=budget_s,
@@ -280,6 +297,7 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "gpu_launches": res.device["window_loop_launches"],
             "clocks": clocks,
+            "interpreter": interp_line(res, c, world),
             "init_ms": {"create_population": res.timings.create_population_ms,
                         "compute_semantics": res.timings.compute_semantics_ms,
                         **res.device["init_ms"]},

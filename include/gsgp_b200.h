@@ -76,7 +76,8 @@ typedef struct gsgp_outputs {
                                     12 upload (H2D + transpose), 13 interpret population,
                                     14 interpret pool, 15 initial SSE (sums over shards),
                                     16 genome compile, 17 device allocation + clears (host
-                                    clock), 18-19 reserved */
+                                    clock), 18 / 19 total compiled instructions (counts, not ms)
+                                    of the population / random-tree programs */
 } gsgp_outputs;
 
 const char* gsgp_version(void);

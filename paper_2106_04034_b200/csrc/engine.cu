@@ -407,6 +407,10 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   GSGP_CUDA(cudaEventRecord(ev_compile1.e, st));
   int32_t maxima[3] = {0, 0, 0};   // {spill depth, constants, instructions}
   GSGP_CUDA(cudaMemcpyAsync(maxima, pmax.p, 12, cudaMemcpyDeviceToHost, st));
+  // program lengths: one instruction per function node of the compiled tree
+  // (the interpreter's work unit, reported as node evaluations per second)
+  std::vector<int32_t> hlen(ng);
+  GSGP_CUDA(cudaMemcpyAsync(hlen.data(), plen.p, ng * 4, cudaMemcpyDeviceToHost, st));
   GSGP_CUDA(cudaStreamSynchronize(st));
 
   // ---- per shard: upload the case slice, interpret population and pool
@@ -766,6 +770,10 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   for (int q = 0; q < 4; ++q) out->stage_ms[12 + q] = init_phase_ms[q];
   out->stage_ms[16] = elapsed_ms(ev_compile0, ev_compile1);
   out->stage_ms[17] = alloc_ms;
+  double ins_pop = 0, ins_pool = 0;
+  for (int64_t i = 0; i < ng; ++i) (i < m ? ins_pop : ins_pool) += hlen[i];
+  out->stage_ms[18] = ins_pop;    // instructions (not ms): population programs
+  out->stage_ms[19] = ins_pool;   // instructions: random-tree programs
 }
 
 }  // namespace gsgp

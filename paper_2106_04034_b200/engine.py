@@ -127,6 +127,7 @@ def run_evolution(cfg: RunConfig, train: Dataset, test: Dataset, *, storage: str
               "init_ms": {"upload": st[12], "interpret_population": st[13],
                           "interpret_pool": st[14], "initial_sse": st[15], "compile": st[16],
                           "alloc": st[17]},
+              "program_instructions": {"population": int(st[18]), "pool": int(st[19])},
               "storage": storage}
     return RunResult(
         config=cfg, train_fitness=a["train_trace"], test_fitness=a["test_trace"], lineage=log,
