@@ -384,11 +384,16 @@ __global__ void __launch_bounds__(NT) k_interpret(InterpArgs a, int64_t gpb,
       double x[CPT];
       fetch(in.y, in.w, x);
       const uint32_t kind = in.x & 0xff;
-      double y[CPT];
-      if (kind >= K_LADD) fetch(in.z, (in.x & 0x100) ? 0xffffffffu : 0u, y);   // second leaf
       // one warp-uniform jump (interp_dispatch.inc); each arm is straight-line
       // code over the CPT cases of this thread, one IEEE rounding per case
-      Dispatch<CPT, CSTRIDE>::run(acc, x, y, kind, in.x, sp0, a.eps, dlo);
+      if constexpr (kXSmem && !kLean && CPT != 1) {
+        // leaf-pair arms fetch their second operand themselves
+        DispatchY<CPT, CSTRIDE>::run(acc, x, kind, in.x, sp0, a.eps, dlo, in.z, sbase, tid8);
+      } else {
+        double y[CPT];
+        if (kind >= K_LADD) fetch(in.z, (in.x & 0x100) ? 0xffffffffu : 0u, y);   // second leaf
+        Dispatch<CPT, CSTRIDE>::run(acc, x, y, kind, in.x, sp0, a.eps, dlo);
+      }
     }
     // ---- epilogue: non-finite -> 0.0 counted (core.py:348-356), then store
     double sse_tr = 0.0, sse_te = 0.0;
