@@ -97,9 +97,9 @@ enum InsClass : uint32_t { X_FEAT = 0, X_CONST = 1, X_STACK = 2 };
 struct __align__(16) Ins {
   // abstract (compile): a = kind | x class << 8 | y class << 12 | push slot << 16,
   //                     b = x index, c = y index (L*/P* kinds)
-  // linked (interpret): a = kind | y-is-vector << 8 | push slot << 16,
-  //                     b = x byte offset, c = y byte offset (L*/P*),
-  //                     d = x lane mask (~0 vector row, 0 broadcast constant);
+  // linked (interpret): a = kind, b = x byte offset, c = y byte offset (L*/P*),
+  //                     d = x lane mask (0x3ff vector row, 0 broadcast constant)
+  //                         | y-is-vector << 16 | push slot << 20;
   //                     feature offsets carry kFeatGlobal when features stay in HBM,
   //                     constants kConstGlobal in the lean (huge-program) configuration
   uint32_t a, b, c, d;

@@ -261,9 +261,11 @@ __global__ void k_link(const Ins* __restrict__ code, Ins* __restrict__ exe, cons
     uint32_t xvec, yvec = 0;
     Ins o;
     o.b = off(xcls, in.b, xvec);
-    o.d = xvec ? 0xffffffffu : 0u;
     o.c = kind >= K_LADD ? off(ycls, in.c, yvec) : 0u;
-    o.a = kind | (yvec << 8) | (push << 16);
+    o.a = kind;
+    // d: x lane mask in the low bits (tid*8 < 1024), y-is-vector bit 16,
+    // push slot from bit 20 — so the interpreter uses a as the jump index as is
+    o.d = (xvec ? 0x3ffu : 0u) | (yvec << 16) | (push << 20);
     exe[g * k1 + i] = o;
   }
 }
@@ -383,16 +385,16 @@ __global__ void __launch_bounds__(NT) k_interpret(InterpArgs a, int64_t gpb,
       nxt = kLean ? __ldg(gprog + i + 1) : lds_u128(pbase + (uint32_t)(i + 1) * 16u);
       double x[CPT];
       fetch(in.y, in.w, x);
-      const uint32_t kind = in.x & 0xff;
+      const uint32_t kind = in.x;
       // one warp-uniform jump (interp_dispatch.inc); each arm is straight-line
       // code over the CPT cases of this thread, one IEEE rounding per case
       if constexpr (kXSmem && !kLean && CPT != 1) {
         // leaf-pair arms fetch their second operand themselves
-        DispatchY<CPT, CSTRIDE>::run(acc, x, kind, in.x, sp0, a.eps, dlo, in.z, sbase, tid8);
+        DispatchY<CPT, CSTRIDE>::run(acc, x, kind, in.w, sp0, a.eps, dlo, in.z, sbase, tid8);
       } else {
         double y[CPT];
-        if (kind >= K_LADD) fetch(in.z, (in.x & 0x100) ? 0xffffffffu : 0u, y);   // second leaf
-        Dispatch<CPT, CSTRIDE>::run(acc, x, y, kind, in.x, sp0, a.eps, dlo);
+        if (kind >= K_LADD) fetch(in.z, (in.w & 0x10000u) ? 0xffffffffu : 0u, y);   // second leaf
+        Dispatch<CPT, CSTRIDE>::run(acc, x, y, kind, in.w, sp0, a.eps, dlo);
       }
     }
     // ---- epilogue: non-finite -> 0.0 counted (core.py:348-356), then store
