@@ -53,6 +53,9 @@ def test_random_run_matches_engine_restatement(seed, monkeypatch):
     kw, Xtr, ytr, Xte, yte = _random_case(seed)
     if seed % 4 == 1:
         monkeypatch.setenv("GSGP_UPLOAD_CHUNK", "3072")
+    # every interpreter launch configuration takes part (0 128x4, 2 HBM
+    # features, 3 128x2, 4 lean, 5 128x3 default)
+    monkeypatch.setenv("GSGP_INTERP_CFG", "05234"[seed % 5])
     res = G.run_evolution(G.RunConfig(**kw), G.Dataset(Xtr, ytr), G.Dataset(Xte, yte),
                           virtual_shards=1 + seed % 3)
     o = engine32.run32(R.Cfg(**kw), Xtr, ytr, Xte, yte)
@@ -75,3 +78,19 @@ def test_random_run_fp64_storage_matches_reference_loop(seed):
     np.testing.assert_allclose(res.train_fitness, o["train"], rtol=1e-12, atol=0)
     np.testing.assert_allclose(res.test_fitness, o["test"], rtol=1e-12, atol=0)
     np.testing.assert_allclose(res.elite_train_semantics, o["elite_train_semantics"], rtol=1e-12, atol=1e-300)
+
+
+def test_wide_feature_run_matches_engine_restatement(monkeypatch):
+    """150 features (features stay in HBM, 3072-case upload chunks) through a
+    whole run: plans, elite records and elite semantics exact."""
+    rng = np.random.default_rng(77)
+    l, ntr, nte = 150, 6000, 1500
+    Xtr, Xte = rng.uniform(-1, 1, (ntr, l)), rng.uniform(-1, 1, (nte, l))
+    ytr, yte = Xtr[:, 0] * Xtr[:, 7] + Xtr[:, 149], Xte[:, 0] * Xte[:, 7] + Xte[:, 149]
+    kw = dict(population_size=40, random_trees=24, program_size=255, generations=6, seed=5)
+    monkeypatch.setenv("GSGP_UPLOAD_CHUNK", "3072")
+    res = G.run_evolution(G.RunConfig(**kw), G.Dataset(Xtr, ytr), G.Dataset(Xte, yte))
+    o = engine32.run32(R.Cfg(**kw), Xtr, ytr, Xte, yte)
+    assert _elite(res) == [e[:3] for e in o["elite"]]
+    np.testing.assert_allclose(res.train_fitness, o["train"], rtol=1e-12, atol=0)
+    assert np.array_equal(res.elite_train_semantics, o["elite_train_semantics"])
