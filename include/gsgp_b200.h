@@ -87,7 +87,8 @@ const char* gsgp_last_error(void);
 int gsgp_device_info(int* device_count, int* sm_count, char* name, int name_len);
 int gsgp_set_device(int device);
 /* Return the engine's cached device memory (a run parks its device blocks
-   for the next run instead of freeing them) to the driver.  No reference
+   for the next run instead of freeing them) and its pinned upload staging
+   to the driver.  No reference
    counterpart: the reference allocates with numpy per call. */
 int gsgp_trim_device_memory(void);
 

@@ -191,8 +191,6 @@ void comm_init(int world, int rank, const unsigned char* id) {
   nccl().check(nccl().commInitRank(&c.comm, world, u, rank), "ncclCommInitRank");
 }
 
-void trim_device_memory() { cache_trim(); }
-
 void comm_init_host(int world, int rank, HostAllreduce fn) {
   GSGP_REQUIRE(world >= 1 && rank >= 0 && rank < world && fn, "bad world/rank/callback");
   CommState& c = comm_state();
@@ -273,8 +271,12 @@ struct PinnedStage {
   void* p = nullptr;
   size_t bytes = 0;
 };
-PinnedStage& pinned_stage(size_t bytes) {
+PinnedStage& pinned_stage_ref() {
   static PinnedStage s;
+  return s;
+}
+PinnedStage& pinned_stage(size_t bytes) {
+  PinnedStage& s = pinned_stage_ref();
   // allocate the full double buffer on first use (page-locking ~100 MB costs
   // ~50 ms; growing it run by run would charge that to later runs)
   if (bytes < 2 * kUploadChunkBytes + (64u << 10)) bytes = 2 * kUploadChunkBytes + (64u << 10);
@@ -286,6 +288,14 @@ PinnedStage& pinned_stage(size_t bytes) {
     s.bytes = bytes;
   }
   return s;
+}
+
+void trim_device_memory() {
+  cache_trim();
+  PinnedStage& ps = pinned_stage_ref();
+  if (ps.p) cudaFreeHost(ps.p);
+  ps.p = nullptr;
+  ps.bytes = 0;
 }
 
 struct Shard {
