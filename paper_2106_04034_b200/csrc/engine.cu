@@ -676,7 +676,13 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
       ++n;
     } else {
       for (auto& p : sh) {
-        if (p->pitch == 0) continue;
+        if (p->pitch == 0) {
+          // an empty case slice contributes zeros; its SSE vector must be
+          // cleared every generation because (single local shard) it is also
+          // the in-place allreduce buffer that held last generation's sum
+          GSGP_CUDA(cudaMemsetAsync(p->sse.p, 0, m * 2 * 8, s));
+          continue;
+        }
         launch_reduce_partials(p->part.as<double>(), m, p->ntiles, p->sse.as<double>(), false, s);
         ++n;
       }

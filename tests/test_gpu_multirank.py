@@ -50,7 +50,8 @@ def _worker(rank, world, port, name, vshards, q):
         td.destroy_process_group()
 
 
-@pytest.mark.parametrize("name,world,vshards", [("accept", 2, 1), ("c1", 3, 1), ("c2s", 2, 2)])
+@pytest.mark.parametrize("name,world,vshards", [("accept", 2, 1), ("c1", 3, 1), ("c2s", 2, 2), ("wide", 2, 1),
+                                                 ("n1", 2, 1)])
 def test_ranks_sharing_a_gpu_reproduce_single_process_run(name, world, vshards):
     import paper_2106_04034_b200 as G
     g = golden(name)
