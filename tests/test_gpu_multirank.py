@@ -125,3 +125,57 @@ def test_replica_runs_across_ranks_match_sequential_runs():
         assert p.exitcode == 0
     assert got[0][1] == [0, 2, 4] and got[1][1] == [1, 3]
     assert got[0][2] == seq
+
+
+def _case(seed, tiny):
+    from test_gpu_random_runs import _random_case
+    kw, Xtr, ytr, Xte, yte = _random_case(seed)
+    if tiny:                      # fewer cases than ranks: some slices are empty
+        a, b = 1 + seed % 2, 1 + seed % 3
+        Xtr, ytr, Xte, yte = Xtr[:a], ytr[:a], Xte[:b], yte[:b]
+    return kw, Xtr, ytr, Xte, yte
+
+
+def _random_worker(rank, world, port, seed, vshards, tiny, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    td.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2106_04034_b200 as G
+        from paper_2106_04034_b200 import dist
+        dist.init_host_exchange()
+        kw, Xtr, ytr, Xte, yte = _case(seed, tiny)
+        res = G.run_evolution(G.RunConfig(**kw), G.Dataset(Xtr, ytr), G.Dataset(Xte, yte),
+                              virtual_shards=vshards)
+        full = dist.gather_elite_semantics(res, Xtr.shape[0])
+        q.put((rank, [(e.elite.source, e.elite.index, e.elite.slot) for e in res.lineage.entries],
+               res.train_fitness.tolist(), full.tolist()))
+        dist.destroy()
+    finally:
+        td.destroy_process_group()
+
+
+@pytest.mark.parametrize("seed,world,vshards,tiny",
+                         [(s, 2 + s % 3, 1 + s % 2, s >= 204) for s in range(200, 210)])
+def test_random_configs_across_ranks(seed, world, vshards, tiny):
+    """Random configurations (tiny case counts included, so some ranks hold
+    no cases) over 2-4 ranks x 1-2 virtual shards == the single-process run."""
+    import paper_2106_04034_b200 as G
+    kw, Xtr, ytr, Xte, yte = _case(seed, tiny)
+    one = G.run_evolution(G.RunConfig(**kw), G.Dataset(Xtr, ytr), G.Dataset(Xte, yte))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_random_worker, args=(r, world, port, seed, vshards, tiny, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    got = sorted(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    one_elite = [(e.elite.source, e.elite.index, e.elite.slot) for e in one.lineage.entries]
+    for rank, elite, train, full in got:
+        assert elite == one_elite, (rank, kw)
+        np.testing.assert_allclose(train, one.train_fitness, rtol=1e-12, atol=0)
+        assert np.array_equal(np.array(full), one.elite_train_semantics)
