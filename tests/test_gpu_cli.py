@@ -95,3 +95,40 @@ def test_bench_cli_program_size_sweep(tmp_path):
         "create_population", "compute_semantics", "generation", "total"}
     sem = [float(r["millis"]) for r in rows if r["stage"] == "compute_semantics"]
     assert sem[0] < sem[1] < sem[2]
+
+
+def _cli_rank(rank, world, port, out_dir, q):
+    import os
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank), GSGP_SHARED_GPU="1")
+    import paper_2106_04034_b200 as G2
+    code = G2.run_cli(["-train_file", str(REF / "train.txt"), "-test_file", str(REF / "test.txt"),
+                       "-config", str(REF / "config.ini"), "-output_dir", str(out_dir), "-backend", "cuda"])
+    import torch.distributed as td
+    if td.is_initialized():
+        td.destroy_process_group()
+    q.put((rank, code))
+
+
+def test_cli_replicas_over_two_ranks_match_single_process(tmp_path):
+    """gsgp-run under 2 ranks (runs as replicas, both ranks on this GPU):
+    trace files in run order and sidecars identical to the one-process CLI."""
+    import socket
+
+    import torch.multiprocessing as mp
+    one = _cli(tmp_path)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    out2 = tmp_path / "rep"
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_cli_rank, args=(r, 2, port, out2, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    codes = sorted(q.get(timeout=600) for _ in range(2))
+    for p in procs:
+        p.join(timeout=120)
+    assert codes == [(0, 0), (1, 0)]
+    for name in ("fitnesstrain.txt", "fitnesstest.txt", "lineage_run000.txt", "lineage_run001.txt"):
+        assert (out2 / name).read_text() == (one / name).read_text(), name
