@@ -63,6 +63,14 @@ def unit_vec(seed: int, stream: int, counters) -> np.ndarray:
     return (z >> np.uint64(11)).astype(np.float64) * TWO_M53
 
 
+def split_rows(n: int, train_fraction: float, seed: int):
+    """Row indices of Dataset.split (R:core.py:179-192): stable argsort of the
+    split-stream uniforms, first round(n*f) (clamped to [1, n-1]) rows train."""
+    order = np.argsort(unit_vec(seed, SPLIT_STREAM, np.arange(n)), kind="stable")
+    cut = max(1, min(n - 1, round(n * train_fraction)))
+    return order[:cut], order[cut:]
+
+
 def run_seed(seed: int, index: int) -> int:
     """Seed of sub-run `index` (R:rng.py:67-69)."""
     return finalize((finalize(seed ^ STREAM_MULT) + (index & M64) * GOLDEN) & M64)

@@ -305,7 +305,21 @@ def gen_cli():
     (out / "timings.csv").unlink()   # wall-clock values: not a fixture
 
 
+def gen_split():
+    """Dataset.split (gsgp/core.py:179-192): rows of each side for several
+    sizes, fractions and seeds (the row ids are stored as feature column 0)."""
+    rows = {}
+    for n, frac, seed in ((2, 0.5, 1), (10, 0.7, 3), (37, 0.25, 5), (1000, 0.8, -7), (513, 0.999, 2**40)):
+        X = np.stack([np.arange(n, dtype=np.float64), np.ones(n)], axis=1)
+        tr, te = gsgp.Dataset(X, np.arange(n, dtype=np.float64)).split(frac, seed)
+        rows[f"tr_{n}"] = tr.features[:, 0].astype(np.int64)
+        rows[f"te_{n}"] = te.features[:, 0].astype(np.int64)
+        rows[f"args_{n}"] = np.array([frac, seed], dtype=object)
+    np.savez_compressed(OUT / "split.npz", **rows)
+
+
 if __name__ == "__main__":
+    gen_split()
     gen_rng()
     gen_population()
     gen_interpreter()

@@ -401,3 +401,16 @@ def test_interpreter_division_fast_path_near_halfway_quotients():
         finally:
             del os.environ["GSGP_INTERP_CFG"]
         assert np.array_equal(S.view(np.uint64), ref.view(np.uint64)), cfg
+
+
+def test_dataset_split_matches_reference_golden():
+    """Dataset.split (gsgp/core.py:179-192) with device-drawn uniforms: the
+    same rows on each side as the reference for several sizes and seeds."""
+    g = golden("split")
+    for key in [k for k in g.files if k.startswith("tr_")]:
+        n = int(key[3:])
+        frac, seed = g[f"args_{n}"]
+        X = np.stack([np.arange(n, dtype=np.float64), np.ones(n)], axis=1)
+        tr, te = G.Dataset(X, np.arange(n, dtype=np.float64)).split(float(frac), int(seed))
+        assert np.array_equal(tr.features[:, 0].astype(np.int64), g[f"tr_{n}"]), n
+        assert np.array_equal(te.features[:, 0].astype(np.int64), g[f"te_{n}"]), n

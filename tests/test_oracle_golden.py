@@ -104,3 +104,12 @@ def test_full_run_bit_exact(name):
     assert out["overflow"] == int(g["overflow"][0])
     if "u" in g.files:
         assert np.array_equal(out["u"], g["u"]) and np.array_equal(out["ms"], g["ms"])
+
+
+def test_split_restatement_matches_reference():
+    g = golden("split")
+    for key in [k for k in g.files if k.startswith("tr_")]:
+        n = int(key[3:])
+        frac, seed = g[f"args_{n}"]
+        tr, te = R.split_rows(n, float(frac), int(seed))
+        assert np.array_equal(tr, g[f"tr_{n}"]) and np.array_equal(te, g[f"te_{n}"]), n
