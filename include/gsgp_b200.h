@@ -144,24 +144,37 @@ int gsgp_sigmoid(const double* x, int64_t n, double* out);
  * argmax}, ties to the lowest index */
 int gsgp_argminmax(const double* fitness, int64_t m, int64_t* out);
 
+/* The engine's canonical SSE sum of non-negative fp64 partials (the
+ * reduction behind every fitness of gsgp_run; no reference counterpart —
+ * replaces the row sums of gsgp/fitness.py:23 across tiles and ranks):
+ * out[i] = sum_j x[i][j], rounded once from an exact fixed-point sum
+ * anchored on the row's largest exponent, so the result does not depend on
+ * the order or grouping of the x[i][j].  parts = 0 runs the fused
+ * single-shard path, parts >= 1 splits the columns into that many pieces
+ * and runs the multi-shard path (anchors, digits, finish). */
+int gsgp_canonical_sum(const double* x, int64_t rows, int64_t n, int32_t parts, double* out);
+
 /* run_evolution (gsgp/evolution.py:100-179) */
 int gsgp_run(const gsgp_config* cfg, const double* Xtr, const double* ytr, int64_t ntr,
              const double* Xte, const double* yte, int64_t nte, int32_t n_features,
              gsgp_outputs* out);
 
 /* Multi-GPU: one process per GPU.  Rank 0 creates the id, every rank calls
- * gsgp_comm_init with it; gsgp_run then shards the cases across ranks and
- * allreduces the per-row partial SSE each generation (NCCL over NVLink). */
+ * gsgp_comm_init with it; gsgp_run then shards the cases across ranks
+ * (slices aligned to 12288 cases) and allreduces each generation the rows'
+ * canonical-SSE anchors (int32 max) and digit sums (uint64 sum) over NCCL:
+ * results are bit-identical for any number of ranks. */
 int gsgp_comm_unique_id(unsigned char id[128]);
 int gsgp_comm_init(int world, int rank, const unsigned char id[128]);
-/* Test transport for the same collectives: `allreduce` sums a HOST buffer
-   of `count` elements (dtype 0 fp64, 1 int32, 2 uint64) over the ranks in
-   place (e.g. torch.distributed over gloo), so the multi-rank engine path
-   runs with several processes sharing one GPU.  Runs use direct launches
-   (no graph) in this mode. */
+/* Test transport for the same collectives: `allreduce` reduces a HOST
+   buffer of `count` elements over the ranks in place (e.g. torch.distributed
+   over gloo); dtype 0 = fp64 sum, 1 = int32 sum, 2 = uint64 sum, 3 = int32
+   max.  The multi-rank engine path then runs with several processes sharing
+   one GPU.  Runs use direct launches (no graph) in this mode. */
 int gsgp_comm_init_host(int world, int rank, void (*allreduce)(void* buf, int64_t count, int32_t dtype));
 int gsgp_comm_destroy(void);
-/* contiguous case slice [lo, hi) of shard `index` out of `count` */
+/* contiguous case slice [lo, hi) of shard `index` out of `count`; interior
+ * boundaries are multiples of 12288 cases (the canonical SSE tile grid) */
 void gsgp_shard_range(int64_t n, int64_t count, int64_t index, int64_t* lo, int64_t* hi);
 
 #ifdef __cplusplus

@@ -18,7 +18,7 @@ from .core import (
 )
 from .engine import GenerationState, RunResult, replay_lineage, run_evolution, survive
 from .ops import (
-    argmax_fitness, argmin_fitness, build_mutation_plan, compute_fitness, compute_semantics,
+    argmax_fitness, argmin_fitness, build_mutation_plan, canonical_sum, compute_fitness, compute_semantics,
     create_population, derive_seed, gsm, gsm_paired, gsm_step_f32, interpret,
     release_device_memory, rmse, rng_bits, rng_stream, sample_gene, sigmoid, sigmoid_array,
     uniform_array,

@@ -30,7 +30,7 @@ EXPORTS = (
     "gsgp_build_mutation_plan", "gsgp_gsm", "gsgp_gsm_step_f32", "gsgp_survive", "gsgp_run",
     "gsgp_comm_unique_id", "gsgp_comm_init", "gsgp_comm_init_host", "gsgp_comm_destroy",
     "gsgp_shard_range",
-    "gsgp_sigmoid", "gsgp_argminmax",
+    "gsgp_sigmoid", "gsgp_argminmax", "gsgp_canonical_sum",
 )
 
 
@@ -92,6 +92,7 @@ _SIGS = {
     "gsgp_shard_range": (None, [I64, I64, I64, P, P]),
     "gsgp_sigmoid": (C.c_int, [P, I64, P]),
     "gsgp_argminmax": (C.c_int, [P, I64, P]),
+    "gsgp_canonical_sum": (C.c_int, [P, I64, I64, I32, P]),
 }
 
 

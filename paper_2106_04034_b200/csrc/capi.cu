@@ -7,6 +7,8 @@
 #include <vector>
 
 #include "gsgp_b200.h"
+#include <memory>
+
 #include "kernels.cuh"
 
 namespace gsgp {
@@ -219,6 +221,7 @@ int gsgp_compute_semantics(const uint8_t* tags, const int32_t* codes, const doub
     a.l = l;
     a.ntr = n;
     a.nte = 0;
+    a.te_q = n;
     a.q_base = 0;
     a.nq = n;
     a.eps = eps;
@@ -291,7 +294,7 @@ int gsgp_gsm(const double* parent, int64_t m, int64_t n, const double* trees, in
     h2d(du.p, u, m * 8);
     h2d(dv.p, v, m * 8);
     h2d(dm.p, ms, m * 8);
-    const int64_t ntiles = gsm_tiles(pitch, true);
+    const int64_t ntiles = gsm_tiles(pitch, pitch, true);
     Buf part(m * ntiles * 2 * 8);
     GsmArgs a{};
     a.pool = T.p;
@@ -349,7 +352,7 @@ int gsgp_gsm_step_f32(const float* parent_tr, const float* parent_te, const floa
     h2d(du.p, u, m * 8);
     h2d(dv.p, v, m * 8);
     h2d(dm.p, ms, m * 8);
-    const int64_t ntiles = gsm_tiles(pitch, false);
+    const int64_t ntiles = gsm_tiles(pitch, toff, false);
     Buf part(m * ntiles * 2 * 8);
     GsmArgs a{};
     a.pool = T.p;
@@ -369,7 +372,7 @@ int gsgp_gsm_step_f32(const float* parent_tr, const float* parent_te, const floa
     GSGP_CUDA(cudaMemset(ticket.p, 0, 16));
     a.ticket = ticket.as<unsigned long long>();
     launch_gsm(a, false, false, 0);
-    launch_reduce_partials(part.as<double>(), m, ntiles, sse.as<double>(), false, 0);
+    launch_reduce_partials(part.as<double>(), m, ntiles, sse.as<double>(), 0);
     GSGP_CUDA(cudaMemcpy2D(out_tr, ntr * 4, P.p, pitch * 4, ntr * 4, m, cudaMemcpyDeviceToHost));
     if (nte > 0)
       GSGP_CUDA(cudaMemcpy2D(out_te, nte * 4, P.as<float>() + toff, pitch * 4, nte * 4, m,
@@ -415,6 +418,43 @@ int gsgp_argminmax(const double* f, int64_t m, int64_t* out) {
     h2d(a.p, f, m * 8);
     launch_argminmax(a.as<double>(), m, o.as<int64_t>(), 0);
     d2h(out, o.p, 2 * 8);
+  });
+}
+
+int gsgp_canonical_sum(const double* x, int64_t rows, int64_t n, int32_t parts, double* out) {
+  return guarded([&] {
+    require_device();
+    GSGP_REQUIRE(rows >= 1 && n >= 1 && parts >= 0, "bad canonical sum shape");
+    // x[row][j] -> the engine's partial layout part[row][j][2] (train slot)
+    std::vector<double> h(rows * n * 2, 0.0);
+    for (int64_t i = 0; i < rows * n; ++i) h[2 * i] = x[i];
+    Buf part(rows * n * 16), sse(rows * 16);
+    h2d(part.p, h.data(), rows * n * 16);
+    if (parts == 0) {   // single part: the fused one-warp-per-row path
+      launch_reduce_partials(part.as<double>(), rows, n, sse.as<double>(), 0);
+    } else {            // columns split into `parts` pieces: the multi-shard path
+      const int64_t w = (n + parts - 1) / parts;
+      std::vector<std::unique_ptr<Buf>> pieces;
+      Buf cexp(rows * 2 * 4), cdig(rows * 2 * kLimbs * 8);
+      launch_canon_clear(rows, cexp.as<int32_t>(), cdig.as<unsigned long long>(), 0);
+      for (int64_t c0 = 0; c0 < n; c0 += w) {
+        const int64_t nc = std::min(w, n - c0);
+        pieces.push_back(std::make_unique<Buf>(rows * nc * 16));
+        GSGP_CUDA(cudaMemcpy2D(pieces.back()->p, nc * 16, h.data() + 2 * c0, n * 16, nc * 16, rows,
+                               cudaMemcpyHostToDevice));
+        launch_canon_exp(pieces.back()->as<double>(), rows, nc, cexp.as<int32_t>(), 0);
+      }
+      int64_t c0 = 0;
+      for (auto& b : pieces) {
+        const int64_t nc = std::min(w, n - c0);
+        launch_canon_digits(b->as<double>(), rows, nc, cexp.as<int32_t>(), cdig.as<unsigned long long>(), 0);
+        c0 += w;
+      }
+      launch_canon_finish(cexp.as<int32_t>(), cdig.as<unsigned long long>(), rows, sse.as<double>(), 0);
+    }
+    std::vector<double> r(rows * 2);
+    d2h(r.data(), sse.p, rows * 16);
+    for (int64_t i = 0; i < rows; ++i) out[i] = r[2 * i];
   });
 }
 

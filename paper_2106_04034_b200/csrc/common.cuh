@@ -152,4 +152,86 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// ------------------------------------------- canonical (order-free) SSE sums
+// The SSE of a row is summed from fp64 tile partials (tiles anchored on
+// global case positions, see engine.cu shard_range).  Adding the partials in
+// floating point would make the result depend on how the tiles are split
+// across shards and ranks; instead every partial v >= 0 is converted to a
+// fixed-point integer X = floor(v * 2^(116 - A)) anchored on the row's largest
+// partial exponent A (an exact max over all shards/ranks), the integers are
+// summed exactly (u64 limbs of 32-bit digits: integer adds, any order, any
+// NCCL reduction tree), and the total is rounded once to fp64.  The result is
+// therefore a function of the multiset of partials only: bit-identical for
+// any number of GPUs and virtual shards.  Truncated bits are < 2^(A-116) per
+// partial, i.e. < ntiles * 2^-116 relative to the sum.
+constexpr int kLimbs = 4;                      // digits 0..3 of X (X < 2^117)
+constexpr int32_t kExpZero = -0x7f7f7f80;      // no non-zero partial (memset 0x80 is below it)
+constexpr int32_t kExpInf = 0x7ffffff0;        // some partial is +inf
+constexpr int32_t kExpNaN = 0x7fffffff;        // some partial is NaN
+constexpr int kAnchor = 116;
+
+__device__ __forceinline__ int32_t canon_exp(double v) {
+  if (v != v) return kExpNaN;
+  if (v == 0.0) return kExpZero;
+  if (isinf(v)) return kExpInf;
+  const uint64_t b = (uint64_t)__double_as_longlong(v);
+  const int32_t ef = (int32_t)((b >> 52) & 0x7ff);
+  if (ef) return ef - 1023;
+  return -1074 + 63 - __clzll((long long)(b & ((1ull << 52) - 1)));   // subnormal
+}
+
+// add the digits of floor(v * 2^(kAnchor - A)) to L (A = canon_exp max, finite)
+__device__ __forceinline__ void canon_add(double v, int32_t A, unsigned long long L[kLimbs]) {
+  if (!(v > 0.0)) return;
+  const uint64_t b = (uint64_t)__double_as_longlong(v);
+  const int32_t ef = (int32_t)((b >> 52) & 0x7ff);
+  const uint64_t M = (b & ((1ull << 52) - 1)) | (ef ? (1ull << 52) : 0ull);
+  const int32_t sh = (ef ? ef - 1075 : -1074) + kAnchor - A;   // X = M * 2^sh, sh <= 64
+  unsigned __int128 X;
+  if (sh >= 0) X = (unsigned __int128)M << sh;
+  else if (sh > -64) X = M >> (-sh);
+  else return;
+  L[0] += (uint32_t)X;
+  L[1] += (uint32_t)(X >> 32);
+  L[2] += (uint32_t)(X >> 64);
+  L[3] += (uint32_t)(X >> 96);
+}
+
+// round sum(L[d] * 2^(32 d)) * 2^(A - kAnchor) to the nearest fp64 (ties even)
+__device__ __forceinline__ double canon_finish(const unsigned long long L[kLimbs], int32_t A) {
+  if (A == kExpNaN) return __longlong_as_double(0x7ff8000000000000ll);
+  if (A == kExpInf) return __longlong_as_double(0x7ff0000000000000ll);
+  if (A < -1100) return 0.0;
+  unsigned __int128 acc = (unsigned __int128)L[0] + ((unsigned __int128)L[1] << 32);
+  const uint64_t w0 = (uint64_t)acc;
+  acc = (acc >> 64) + (unsigned __int128)L[2] + ((unsigned __int128)L[3] << 32);
+  const uint64_t w1 = (uint64_t)acc, w2 = (uint64_t)(acc >> 64);
+  int h;   // index of the leading bit of the 192-bit integer (w2:w1:w0)
+  if (w2) h = 128 + 63 - __clzll((long long)w2);
+  else if (w1) h = 64 + 63 - __clzll((long long)w1);
+  else if (w0) h = 63 - __clzll((long long)w0);
+  else return 0.0;
+  // top 64 bits starting at the leading one, and whether anything below is set
+  const int lo = h - 63;
+  uint64_t top;
+  bool below = false;
+  if (lo <= 0) {
+    top = w0 << (-lo);
+  } else {
+    const int q = lo >> 6, r = lo & 63;
+    const uint64_t w[4] = {w0, w1, w2, 0};
+    top = r ? (w[q] >> r) | (w[q + 1] << (64 - r)) : w[q];
+    for (int i = 0; i < q; ++i) below |= w[i] != 0;
+    if (r) below |= (w[q] & ((1ull << r) - 1)) != 0;
+  }
+  uint64_t mant = top >> 11;
+  const bool rnd = (top >> 10) & 1;
+  const bool sticky = below || (top & 0x3ff) != 0;
+  int e = h - 52;
+  if (rnd && (sticky || (mant & 1))) {
+    if (++mant == (1ull << 53)) { mant >>= 1; ++e; }
+  }
+  return ldexp((double)mant, e + A - kAnchor);
+}
+
 }  // namespace gsgp

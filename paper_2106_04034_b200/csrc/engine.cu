@@ -153,9 +153,11 @@ NcclApi& nccl() {
 }
 
 // Host exchange (tests): the same collectives through a host callback that
-// sums a host buffer over the ranks (e.g. torch.distributed over gloo), so
-// the multi-rank engine path runs with several processes on one GPU.  dtype:
-// 0 fp64, 1 int32, 2 uint64.  Not graph-capturable: runs use direct launches.
+// reduces a host buffer over the ranks (e.g. torch.distributed over gloo), so
+// the multi-rank engine path runs with several processes on one GPU.  The
+// callback's code (HostRed below): 0 fp64 sum, 1 int32 sum, 2 uint64 sum,
+// 3 int32 max.  Not graph-capturable: runs use direct launches.
+enum HostRed : int32_t { kRedF64Sum = 0, kRedI32Sum = 1, kRedU64Sum = 2, kRedI32Max = 3 };
 typedef void (*HostAllreduce)(void* buf, int64_t count, int32_t dtype);
 
 struct CommState {
@@ -203,22 +205,24 @@ void comm_init_host(int world, int rank, HostAllreduce fn) {
   c.host = fn;
 }
 
-// in-place sum over the ranks of a device buffer on stream s (NCCL or host)
-void allreduce_sum(void* dev, int64_t count, int32_t dtype, cudaStream_t s, const char* what) {
+// in-place reduction over the ranks of a device buffer on stream s (NCCL or host)
+void allreduce(void* dev, int64_t count, HostRed kind, cudaStream_t s, const char* what) {
   CommState& c = comm_state();
   if (c.world <= 1) return;
+  const bool i32 = kind == kRedI32Sum || kind == kRedI32Max;
   if (c.host) {
-    const size_t esz = dtype == 1 ? 4 : 8;
+    const size_t esz = i32 ? 4 : 8;
     std::vector<unsigned char> h(count * esz);
     GSGP_CUDA(cudaMemcpyAsync(h.data(), dev, count * esz, cudaMemcpyDeviceToHost, s));
     GSGP_CUDA(cudaStreamSynchronize(s));
-    c.host(h.data(), count, dtype);
+    c.host(h.data(), count, (int32_t)kind);
     GSGP_CUDA(cudaMemcpyAsync(dev, h.data(), count * esz, cudaMemcpyHostToDevice, s));
     GSGP_CUDA(cudaStreamSynchronize(s));
     return;
   }
-  const ncclDataType_t t = dtype == 0 ? ncclFloat64 : (dtype == 1 ? ncclInt32 : ncclUint64);
-  nccl().check(nccl().allReduce(dev, dev, count, t, ncclSum, c.comm, s), what);
+  const ncclDataType_t t = kind == kRedF64Sum ? ncclFloat64 : (i32 ? ncclInt32 : ncclUint64);
+  const ncclRedOp_t op = kind == kRedI32Max ? ncclMax : ncclSum;
+  nccl().check(nccl().allReduce(dev, dev, count, t, op, c.comm, s), what);
 }
 
 void comm_destroy() {
@@ -230,9 +234,17 @@ void comm_destroy() {
   c.rank = 0;
 }
 
+// Contiguous case slices whose boundaries are multiples of kCaseAlign (the
+// lcm of the generation kernel's case tiles, 4096 / 2048, and every
+// interpreter tile, 128 x {1,2,3,4,8}): each SSE tile partial then covers the
+// same global cases at the same positions for any shard count, and the
+// canonical sum (common.cuh) makes the SSE identical across GPU counts.
+constexpr int64_t kCaseAlign = 12288;
+
 void shard_range(int64_t n, int64_t count, int64_t index, int64_t* lo, int64_t* hi) {
-  *lo = (n * index) / count;
-  *hi = (n * (index + 1)) / count;
+  auto cut = [&](int64_t i) { return i >= count ? n : (n * i) / count / kCaseAlign * kCaseAlign; };
+  *lo = cut(index);
+  *hi = cut(index + 1);
 }
 
 // ------------------------------------------------------------- small kernels
@@ -300,8 +312,8 @@ void trim_device_memory() {
 
 struct Shard {
   int64_t tr_lo = 0, tr_hi = 0, te_lo = 0, te_hi = 0;
-  int64_t ntr = 0, nte = 0, pitch = 0, test_off = 0, ntiles = 0;
-  DevBuf S, pool, elite[2], y_store, part, sse, sse64, ticket;
+  int64_t ntr = 0, nte = 0, pitch = 0, test_off = 0, ntiles = 0, itiles = 0;
+  DevBuf S, pool, elite[2], y_store, part, ipart, ticket;
 };
 
 void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, int64_t ntr,
@@ -356,7 +368,7 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
     p->nte = p->te_hi - p->te_lo;
     p->test_off = pad32(p->ntr);
     p->pitch = p->test_off + pad32(p->nte);
-    p->ntiles = gsm_tiles(p->pitch, f64);
+    p->ntiles = gsm_tiles(p->pitch, p->test_off, f64);
     sh.push_back(std::move(p));
   }
   out->shard_train_lo = sh.front()->tr_lo;
@@ -435,9 +447,6 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
     p->elite[1].alloc(p->pitch * esz);
     p->y_store.alloc(p->pitch * 8);
     p->part.alloc(m * p->ntiles * 2 * 8);
-    p->sse.alloc(m * 2 * 8);
-    p->sse64.alloc(m * 2 * 8);
-    GSGP_CUDA(cudaMemsetAsync(p->sse64.p, 0, m * 2 * 8, st));
     p->ticket.alloc(16);
     GSGP_CUDA(cudaMemsetAsync(p->ticket.p, 0, 16, st));
     GSGP_CUDA(cudaMemsetAsync(p->S.p, 0, m * p->pitch * esz, st));
@@ -445,7 +454,6 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
     GSGP_CUDA(cudaMemsetAsync(p->elite[0].p, 0, p->pitch * esz, st));
     GSGP_CUDA(cudaMemsetAsync(p->elite[1].p, 0, p->pitch * esz, st));
     GSGP_CUDA(cudaMemsetAsync(p->y_store.p, 0, p->pitch * 8, st));
-    GSGP_CUDA(cudaMemsetAsync(p->sse.p, 0, m * 2 * 8, st));
     GSGP_CUDA(cudaStreamSynchronize(st));
     alloc_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_alloc0).count();
     if (N == 0) continue;
@@ -463,6 +471,7 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
     ia.l = l;
     ia.ntr = p->ntr;
     ia.nte = p->nte;
+    ia.te_q = p->ntr;
     ia.eps = cfg->division_eps;
     ia.maxdepth = maxima[0];
     ia.maxconst = maxima[1];
@@ -475,10 +484,15 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
     ia.wide = wide.as<int32_t>();
     ia.nonfinite = nonfinite.as<unsigned long long>();
     int itile = 1;
-    const int64_t itiles = interp_tiles(ia, &itile);
-    DevBuf ipart;
-    ipart.alloc(m * itiles * 2 * 8);
-    ia.part = ipart.as<double>();
+    interp_tiles(ia, &itile);
+    // test cases start on an interpreter tile (stacked index te_q), so no
+    // tile mixes train and test cases: canonical partials (see shard_range)
+    ia.te_q = (p->ntr + itile - 1) / itile * itile;
+    const int64_t itiles = interp_tiles(ia, nullptr);
+    const int64_t Nq = ia.te_q + p->nte;                    // stacked cases incl. the gap
+    p->itiles = itiles;
+    p->ipart.alloc(m * itiles * 2 * 8);
+    ia.part = p->ipart.as<double>();
     ia.part_ntiles = itiles;
     // pool: stream base m, same compiled program buffer offset by m genomes
     InterpArgs ip = ia;
@@ -498,8 +512,8 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
     int64_t chunk = (int64_t)(kUploadChunkBytes / row_bytes) / 3072 * 3072;
     if (const char* e = getenv("GSGP_UPLOAD_CHUNK")) chunk = atoll(e) / 3072 * 3072;   // tests
     if (chunk < 3072) chunk = 3072;
-    if (chunk > N) chunk = (N + itile - 1) / itile * itile;
-    const int64_t nchunks = (N + chunk - 1) / chunk;
+    if (chunk > Nq) chunk = (Nq + itile - 1) / itile * itile;
+    const int64_t nchunks = (Nq + chunk - 1) / chunk;
     PinnedStage& pin = pinned_stage(2 * (size_t)chunk * row_bytes);
     DevBuf Xr[2], XT[2];
     for (int b = 0; b < 2 && b < nchunks; ++b) {
@@ -511,28 +525,34 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
     GSGP_CUDA(cudaEventRecord(e_start.e, st));
     for (int64_t c = 0; c < nchunks; ++c) {
       const int b = (int)(c & 1);
-      const int64_t c0 = c * chunk, nq = std::min(chunk, N - c0);
+      const int64_t c0 = c * chunk, nq = std::min(chunk, Nq - c0);
       double* hx = reinterpret_cast<double*>(pin.p) + (size_t)b * chunk * (l + 1);
       double* hy = hx + (size_t)chunk * l;
       if (c >= 2) GSGP_CUDA(cudaEventSynchronize(ev_h2d[b].e));   // staging buffer b is free
-      // rows [c0, c0 + nq) of the stacked shard (train rows, then test rows)
-      const int64_t ntr_part = std::max<int64_t>(0, std::min(nq, p->ntr - c0));
+      // stacked rows [c0, c0 + nq): train rows [c0, ntr), gap rows [ntr, te_q)
+      // (zero features, never stored or counted), test rows [te_q, Nq)
+      const int64_t tr_end = std::min(c0 + nq, p->ntr);
+      const int64_t ntr_part = std::max<int64_t>(0, tr_end - c0);
+      const int64_t te_beg = std::max(c0, ia.te_q);
+      const int64_t nte_part = std::max<int64_t>(0, c0 + nq - te_beg);
+      const int64_t gap0 = std::max(c0, p->ntr), ngap = std::max<int64_t>(0, std::min(c0 + nq, ia.te_q) - gap0);
       if (ntr_part > 0) {
         std::memcpy(hx, Xtr + (p->tr_lo + c0) * l, ntr_part * l * 8);
         std::memcpy(hy, ytr + p->tr_lo + c0, ntr_part * 8);
       }
-      if (nq > ntr_part) {
-        const int64_t t0 = c0 + ntr_part - p->ntr;          // first test row of the chunk
-        std::memcpy(hx + ntr_part * l, Xte + (p->te_lo + t0) * l, (nq - ntr_part) * l * 8);
-        std::memcpy(hy + ntr_part, yte + p->te_lo + t0, (nq - ntr_part) * 8);
+      if (ngap > 0) std::memset(hx + (gap0 - c0) * l, 0, ngap * l * 8);
+      if (nte_part > 0) {
+        const int64_t t0 = te_beg - ia.te_q;                // first test row of the chunk
+        std::memcpy(hx + (te_beg - c0) * l, Xte + (p->te_lo + t0) * l, nte_part * l * 8);
+        std::memcpy(hy + (te_beg - c0), yte + p->te_lo + t0, nte_part * 8);
       }
       if (c >= 2) GSGP_CUDA(cudaStreamWaitEvent(up, ev_done[b].e, 0));   // device buffers free
       GSGP_CUDA(cudaMemcpyAsync(Xr[b].p, hx, nq * l * 8, cudaMemcpyHostToDevice, up));
       if (ntr_part > 0)
         GSGP_CUDA(cudaMemcpyAsync(p->y_store.as<double>() + c0, hy, ntr_part * 8, cudaMemcpyHostToDevice, up));
-      if (nq > ntr_part)
-        GSGP_CUDA(cudaMemcpyAsync(p->y_store.as<double>() + p->test_off + (c0 + ntr_part - p->ntr),
-                                  hy + ntr_part, (nq - ntr_part) * 8, cudaMemcpyHostToDevice, up));
+      if (nte_part > 0)
+        GSGP_CUDA(cudaMemcpyAsync(p->y_store.as<double>() + p->test_off + (te_beg - ia.te_q),
+                                  hy + (te_beg - c0), nte_part * 8, cudaMemcpyHostToDevice, up));
       GSGP_CUDA(cudaEventRecord(ev_h2d[b].e, up));
       GSGP_CUDA(cudaStreamWaitEvent(st, ev_h2d[b].e, 0));
       k_transpose<<<nblk(nq * l), 256, 0, st>>>(Xr[b].as<double>(), nq, l, XT[b].as<double>());
@@ -554,7 +574,6 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
       GSGP_CUDA(cudaEventRecord(ev_k.back()->e, st));
       GSGP_CUDA(cudaEventRecord(ev_done[b].e, st));
     }
-    launch_reduce_partials(ipart.as<double>(), m, itiles, p->sse64.as<double>(), false, st);
     Event e_sse0, e_sse;
     GSGP_CUDA(cudaEventRecord(e_sse0.e, st));
     // initial SSE of the stored semantics in the generation kernel's order
@@ -570,7 +589,6 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
     ga.part = p->part.as<double>();
     ga.ticket = p->ticket.as<unsigned long long>();
     launch_sse_only(ga, f64, st);
-    launch_reduce_partials(p->part.as<double>(), m, p->ntiles, p->sse.as<double>(), false, st);
     GSGP_CUDA(cudaEventRecord(e_sse.e, st));
     GSGP_CUDA(cudaEventSynchronize(e_sse.e));   // the shard's temporaries are freed at scope end
     init_phase_ms[0] += elapsed_ms(e_start, e_first);      // exposed upload (first chunk)
@@ -579,33 +597,50 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
       init_phase_ms[2] += elapsed_ms(*ev_k[q + 1], *ev_k[q + 2]);
     }
     init_phase_ms[3] += elapsed_ms(e_sse0, e_sse);
-    GSGP_CUDA(cudaStreamSynchronize(st));   // temporaries (Xr, XT, ipart) are freed on scope exit
+    GSGP_CUDA(cudaStreamSynchronize(st));   // temporaries (Xr, XT) are freed on scope exit
   }
 
-  // ---- exchange the initial SSE / overflow flags across shards and ranks
-  // G == 1: survival reads shard 0's SSE vector directly (no copy)
-  DevBuf sse64_total;
+  // ---- canonical SSE over every shard of every rank (common.cuh canon_*):
+  // anchors (max over shards, allreduce-max over ranks), exact digit sums
+  // (over shards, allreduce-sum over ranks), one rounding.  Bit-identical
+  // for any rank / virtual-shard count.
+  DevBuf sse64_total, cexp, cdig;
   sse64_total.alloc(m * 2 * 8);
-  double* sse_vec = G == 1 ? sh[0]->sse.as<double>() : sse_total.as<double>();
-  double* sse64_vec = G == 1 ? sh[0]->sse64.as<double>() : sse64_total.as<double>();
-  auto exchange_of = [&](DevBuf Shard::*mem, double* dst, cudaStream_t s) {
-    if (G > 1) {
-      std::vector<const double*> v;
-      for (auto& p : sh) v.push_back((p.get()->*mem).as<double>());
-      launch_sum_shards(v.data(), G, m * 2, dst, s);
+  cexp.alloc(m * 2 * 4);
+  cdig.alloc(m * 2 * kLimbs * 8);
+  double* sse_vec = sse_total.as<double>();
+  double* sse64_vec = sse64_total.as<double>();
+  auto canon_sse = [&](bool interp_parts, double* dst, cudaStream_t s) {
+    launch_canon_clear(m, cexp.as<int32_t>(), cdig.as<unsigned long long>(), s);
+    for (auto& p : sh) {
+      if (p->pitch == 0) continue;
+      if (interp_parts) launch_canon_exp(p->ipart.as<double>(), m, p->itiles, cexp.as<int32_t>(), s);
+      else launch_canon_exp(p->part.as<double>(), m, p->ntiles, cexp.as<int32_t>(), s);
     }
-    if (W > 1) allreduce_sum(dst, m * 2, 0, s, "ncclAllReduce(sse)");
+    if (W > 1) allreduce(cexp.p, m * 2, kRedI32Max, s, "ncclAllReduce(sse anchors)");
+    for (auto& p : sh) {
+      if (p->pitch == 0) continue;
+      if (interp_parts)
+        launch_canon_digits(p->ipart.as<double>(), m, p->itiles, cexp.as<int32_t>(),
+                            cdig.as<unsigned long long>(), s);
+      else
+        launch_canon_digits(p->part.as<double>(), m, p->ntiles, cexp.as<int32_t>(),
+                            cdig.as<unsigned long long>(), s);
+    }
+    if (W > 1) allreduce(cdig.p, m * 2 * kLimbs, kRedU64Sum, s, "ncclAllReduce(sse digits)");
+    launch_canon_finish(cexp.as<int32_t>(), cdig.as<unsigned long long>(), m, dst, s);
   };
-  auto exchange = [&](cudaStream_t s) { exchange_of(&Shard::sse, sse_vec, s); };
-  exchange(st);
-  exchange_of(&Shard::sse64, sse64_vec, st);
+  canon_sse(false, sse_vec, st);
+  canon_sse(true, sse64_vec, st);
+  GSGP_CUDA(cudaStreamSynchronize(st));
+  for (auto& p : sh) p->ipart.release();
   if (W > 1) {
     DevBuf bits;
     bits.alloc(m * 2 * 4);
     k_wide_split<<<nblk(m), 256, 0, st>>>(wide.as<int32_t>(), m, bits.as<int32_t>());
-    allreduce_sum(bits.p, m * 2, 1, st, "ncclAllReduce(wide)");
+    allreduce(bits.p, m * 2, kRedI32Sum, st, "ncclAllReduce(wide)");
     k_wide_merge<<<nblk(m), 256, 0, st>>>(bits.as<int32_t>(), m, wide.as<int32_t>());
-    allreduce_sum(nonfinite.p, 1, 2, st, "ncclAllReduce(overflow)");
+    allreduce(nonfinite.p, 1, kRedU64Sum, st, "ncclAllReduce(overflow)");
     GSGP_CUDA(cudaStreamSynchronize(st));
   }
 
@@ -640,11 +675,12 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   GSGP_CUDA(cudaMemsetAsync(done.p, 0, 16, st));
   const bool fused_tail = (G == 1 && W == 1);
   // one generation: GSM+SSE with the plan drawn inline (per shard), then the
-  // SSE tile reduction and survival — fused into one kernel when there is a
-  // single shard, else reduce per shard -> exchange -> survive
+  // canonical SSE and survival — fused into one kernel when there is a
+  // single shard, else anchors / digits per shard -> allreduce -> finish -> survive
   auto enqueue_generation = [&](cudaStream_t s, Event* t0, Event* t1) {
     int64_t n = 0;
     if (t0) GSGP_CUDA(cudaEventRecord(t0->e, s));
+    bool plan_written = false;
     for (size_t si = 0; si < sh.size(); ++si) {
       auto& p = sh[si];
       if (p->pitch == 0) continue;
@@ -665,29 +701,24 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
       a.part = p->part.as<double>();
       a.ticket = p->ticket.as<unsigned long long>();
       a.plan_inline = 1;
-      a.write_plan = si == 0 ? 1 : 0;
+      a.write_plan = plan_written ? 0 : 1;   // the first non-empty shard records the plan
+      plan_written = true;
       a.plan = pp;
       launch_gsm(a, f64, false, s);
       ++n;
     }
+    if (!plan_written) {   // no cases on this rank: draw the plan for the lineage record
+      launch_plan(pp, 0, ctl.as<int64_t>(), pu.as<int64_t>(), pv.as<int64_t>(), pms.as<double>(), m, s);
+      ++n;
+    }
     if (t1) GSGP_CUDA(cudaEventRecord(t1->e, s));
-    if (fused_tail && sh[0]->pitch > 0) {
+    if (fused_tail) {
       launch_reduce_survive(sh[0]->part.as<double>(), sh[0]->ntiles, sse_vec, sa, done.as<unsigned int>(), s);
       ++n;
     } else {
-      for (auto& p : sh) {
-        if (p->pitch == 0) {
-          // an empty case slice contributes zeros; its SSE vector must be
-          // cleared every generation because (single local shard) it is also
-          // the in-place allreduce buffer that held last generation's sum
-          GSGP_CUDA(cudaMemsetAsync(p->sse.p, 0, m * 2 * 8, s));
-          continue;
-        }
-        launch_reduce_partials(p->part.as<double>(), m, p->ntiles, p->sse.as<double>(), false, s);
-        ++n;
-      }
-      exchange(s);
-      n += (G > 1) ? 1 : 0;
+      canon_sse(false, sse_vec, s);
+      for (auto& p : sh) n += p->pitch > 0 ? 2 : 0;   // exp + digits per non-empty shard
+      ++n;                                             // finish
       launch_survive(sa, s);
       ++n;
     }

@@ -7,10 +7,11 @@
 // plan in one pass (one row of storage = [train cases | pad | test cases | pad]),
 // followed by the fp64 squared error against the target (gsgp/fitness.py:23).
 // The SSE of each (row, case tile) is reduced in a fixed order —
-// thread-sequential -> warp butterfly -> warps in index order — and the tiles
-// are summed in index order by k_reduce_partials: a function of case positions
-// only, so equal rows get bit-equal SSEs and argmin ties resolve to the
-// lowest index exactly like np.argmin.
+// thread-sequential -> warp butterfly -> warps in index order — and the tile
+// partials are combined by the canonical (exact, order-free) sum of
+// common.cuh: a function of case positions only, so equal rows get bit-equal
+// SSEs, argmin ties resolve to the lowest index exactly like np.argmin, and
+// the result does not depend on how the cases are split over GPUs.
 //
 // Layout / traffic: row-major [rows][pitch] (pitch % 32 == 0).  Parents are
 // updated IN PLACE; the best parent row (ctl[CTL_BP]) is copied aside while
@@ -38,6 +39,19 @@ __device__ __forceinline__ float mut(float p, float a, float b, float ms, int si
 __device__ __forceinline__ double mut(double p, double a, double b, double ms, int sign) {
   double t = sign ? __dadd_rn(a, b) : __dsub_rn(a, b);
   return __dadd_rn(p, __dmul_rn(t, ms));
+}
+
+// Case tiles are anchored separately on the train region [0, test_off) and
+// the test region [test_off, pitch): tiles 0 .. ttr-1 cover train, the rest
+// test, so no tile straddles the two and — with shard slices starting on
+// multiples of kCaseAlign (engine.cu) — every tile holds the same global
+// cases at the same positions for any shard/rank split (canonical partials).
+__device__ __forceinline__ void tile_span(int64_t t, int64_t ttr, int64_t tile, int64_t test_off,
+                                          int64_t pitch, int64_t* off, int64_t* n) {
+  const int64_t o = t < ttr ? t * tile : test_off + (t - ttr) * tile;
+  const int64_t end = t < ttr ? test_off : pitch;
+  *off = o;
+  *n = min(tile, end - o);
 }
 
 // one work unit = (case tile, population row): 16 KB of each streamed row
@@ -136,7 +150,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // offspring that equals its parent bit for bit ties with it, as in numpy).
 template <typename T, bool kOp, bool kSseOnly = false>
 __global__ void __launch_bounds__(kTmaThreads, 1)
-k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t nunits, int kBatch) {
+k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t ttr, int64_t nunits, int kBatch) {
   using Vec = typename Vec16<T>::type;
   constexpr int EV = Vec16<T>::n;
   constexpr int TILE = kTileBytes / (int)sizeof(T);   // elements per unit
@@ -254,8 +268,8 @@ k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t nunits, int kBatch) {
             slot_unit[s] = -1;
             mbar_arrive(full + s);
           } else {
-            const int64_t off = t * TILE;
-            const int64_t n = min((int64_t)TILE, a.pitch - off);
+            int64_t off, n;
+            tile_span(t, ttr, TILE, a.test_off, a.pitch, &off, &n);
             const T* src = (i == redirect) ? elite_prev : S + i * a.pitch;
             const uint32_t bytes = (uint32_t)(n * sizeof(T));
             T* d = data + (int64_t)s * 3 * TILE;
@@ -331,8 +345,8 @@ k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t nunits, int kBatch) {
     }
     const int2 it = slot_it[s];
     const int64_t t = it.y, i = it.x;
-    const int64_t off = t * TILE;
-    const int64_t n = min((int64_t)TILE, a.pitch - off);
+    int64_t off, n;
+    tile_span(t, ttr, TILE, a.test_off, a.pitch, &off, &n);
     if (t != cur_t) {   // target tile: registers, reloaded when the CTA changes tile
 #pragma unroll
       for (int q = 0; q < VPT; ++q) {
@@ -411,10 +425,17 @@ int g_num_sms = 0;
 
 }  // namespace
 
-int64_t gsm_tiles(int64_t pitch, bool f64) {
+int64_t gsm_train_tiles(int64_t test_off, bool f64) {
   const int64_t tile = kTileBytes / (f64 ? 8 : 4);
-  return (pitch + tile - 1) / tile;
+  return (test_off + tile - 1) / tile;
 }
+
+int64_t gsm_tiles(int64_t pitch, int64_t test_off, bool f64) {
+  const int64_t tile = kTileBytes / (f64 ? 8 : 4);
+  return gsm_train_tiles(test_off, f64) + (pitch - test_off + tile - 1) / tile;
+}
+
+int64_t gsm_tile_cases(bool f64) { return kTileBytes / (f64 ? 8 : 4); }
 
 void launch_gsm(const GsmArgs& a, bool f64, bool operator_mode, cudaStream_t s) {
   launch_gsm_mode(a, f64, operator_mode ? 1 : 0, s);
@@ -425,7 +446,9 @@ void launch_sse_only(const GsmArgs& a, bool f64, cudaStream_t s) { launch_gsm_mo
 void launch_gsm_mode(const GsmArgs& a, bool f64, int mode, cudaStream_t s) {
   if (a.m <= 0 || a.pitch <= 0) return;
   GSGP_REQUIRE(a.pitch % 32 == 0, "storage pitch must be a multiple of 32");
-  const int64_t ntiles = gsm_tiles(a.pitch, f64);
+  GSGP_REQUIRE(a.test_off >= 0 && a.test_off <= a.pitch && a.test_off % 32 == 0, "bad test region offset");
+  const int64_t ntiles = gsm_tiles(a.pitch, a.test_off, f64);
+  const int64_t ttr = gsm_train_tiles(a.test_off, f64);
   if (g_num_sms == 0) {
     int dev = 0;
     GSGP_CUDA(cudaGetDevice(&dev));
@@ -444,7 +467,7 @@ void launch_gsm_mode(const GsmArgs& a, bool f64, int mode, cudaStream_t s) {
   if (forced > 0) batch = forced < 32 ? forced : 32;   // one unit per producer lane
   auto go = [&](auto kern) {
     GSGP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
-    kern<<<grid, kTmaThreads, kTmaSmem, s>>>(a, ntiles, nunits, batch);
+    kern<<<grid, kTmaThreads, kTmaSmem, s>>>(a, ntiles, ttr, nunits, batch);
   };
   if (f64) {
     if (mode == 1) go(k_gsm_tma<double, true>);

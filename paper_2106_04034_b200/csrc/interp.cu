@@ -314,9 +314,9 @@ __global__ void __launch_bounds__(NT) k_interpret(InterpArgs a, int64_t gpb,
 #pragma unroll
   for (int c = 0; c < CPT; ++c) {
     const int64_t q = q0 + c * NT + tid;
-    valid[c] = l0 + c * NT + tid < a.nq;
     train[c] = q < a.ntr;
-    col[c] = train[c] ? q : a.test_off + (q - a.ntr);
+    valid[c] = l0 + c * NT + tid < a.nq && (train[c] || q >= a.te_q);   // [ntr, te_q): gap
+    col[c] = train[c] ? q : a.test_off + (q - a.te_q);
     ytr[c] = (MODE == INTERP_POP && valid[c]) ? a.y[col[c]] : 0.0;
   }
   const double* xg = a.XT + l0 + tid;          // global feature rows (!kXSmem)
@@ -449,7 +449,9 @@ void launch_cfg(const InterpArgs& a, cudaStream_t s) {
   constexpr int TILE = NT * CPT;
   constexpr InterpCfg c{NT, CPT, kXSmem, kLean};
   const int64_t ntiles = (a.nq + TILE - 1) / TILE;
-  GSGP_REQUIRE(a.q_base % TILE == 0 && a.q_base + a.nq <= a.ntr + a.nte, "bad interpreter case range");
+  GSGP_REQUIRE(a.te_q >= a.ntr && (a.nte == 0 || a.te_q % TILE == 0 || a.te_q == a.ntr),
+               "test cases must start on an interpreter tile");
+  GSGP_REQUIRE(a.q_base % TILE == 0 && a.q_base + a.nq <= a.te_q + a.nte, "bad interpreter case range");
   const uint32_t rowb = TILE * 8;
   const uint32_t frows = kXSmem ? (uint32_t)a.l : 0u;
   const size_t smem = cfg_smem(c, a);
@@ -499,7 +501,7 @@ int64_t interp_tiles(const InterpArgs& a, int* tile_out) {
   const InterpCfg c = kCfgs[choose_cfg(a)];
   const int64_t tile = (int64_t)c.nt * c.cpt;
   if (tile_out) *tile_out = (int)tile;
-  return (a.ntr + a.nte + tile - 1) / tile;
+  return (a.te_q + a.nte + tile - 1) / tile;
 }
 
 void launch_interpret(const InterpArgs& a, int mode, cudaStream_t s) {

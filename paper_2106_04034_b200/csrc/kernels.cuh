@@ -83,8 +83,10 @@ struct InterpArgs {
   int64_t xt_pitch;
   int32_t l;
   int64_t ntr, nte;         // shard case counts (stacked index q < ntr is train)
+  int64_t te_q;             // stacked index of test case 0 (>= ntr; [ntr, te_q) is a skipped
+                            // gap so the test cases start on a tile: canonical SSE partials)
   int64_t q_base, nq;       // this launch: stacked cases [q_base, q_base + nq) (q_base % tile == 0)
-  int64_t part_ntiles;      // row stride of part[] (tiles over all ntr + nte cases)
+  int64_t part_ntiles;      // row stride of part[] (tiles over all te_q + nte stacked cases)
   double eps;
   // outputs
   double* out64;            // INTERP_F64: [count][ntr+nte]
@@ -98,7 +100,7 @@ struct InterpArgs {
   unsigned long long* nonfinite;   // element count replaced by 0.0
   int32_t raw;              // INTERP_F64 only: keep non-finite values (scalar interpret)
 };
-// case tiles over all ntr + nte cases (the part[] row stride) and the tile size
+// case tiles over all te_q + nte stacked cases (the part[] row stride) and the tile size
 int64_t interp_tiles(const InterpArgs& a, int* tile_out);
 void launch_interpret(const InterpArgs& a, int mode, cudaStream_t s);
 
@@ -116,7 +118,7 @@ struct GsmArgs {
   const double* ms;
   const int64_t* ctl;       // device control block (see engine.cu), may be nullptr
   int32_t sign;             // 0 minus, 1 plus
-  double* part;             // [m][ntiles][2]
+  double* part;             // [m][gsm_tiles][2]
   unsigned long long* nonfinite;   // operator mode only
   // {ticket, exited CTAs}: dynamic unit dispatch; zero before the first
   // launch, the last CTA to exit re-zeroes both for the next launch
@@ -128,7 +130,11 @@ struct GsmArgs {
   int32_t write_plan;
   PlanParams plan;
 };
-int64_t gsm_tiles(int64_t pitch, bool f64);
+// case tiles of a row: train tiles over [0, test_off), then test tiles over
+// [test_off, pitch) (the part[] row stride); cases per tile
+int64_t gsm_tiles(int64_t pitch, int64_t test_off, bool f64);
+int64_t gsm_train_tiles(int64_t test_off, bool f64);
+int64_t gsm_tile_cases(bool f64);
 void launch_gsm(const GsmArgs& a, bool f64, bool operator_mode, cudaStream_t s);
 // SSE of the stored semantics S against y in the generation kernel's exact
 // order (no mutation, no stores): part[m][ntiles][2]
@@ -136,11 +142,18 @@ void launch_sse_only(const GsmArgs& a, bool f64, cudaStream_t s);
 // mode 0 engine, 1 operator (non-finite -> 0), 2 SSE only
 void launch_gsm_mode(const GsmArgs& a, bool f64, int mode, cudaStream_t s);
 
-// sum [rows][ntiles][2] partials (fixed order) into out[rows][2] (+= when accumulate)
-void launch_reduce_partials(const double* part, int64_t rows, int64_t ntiles, double* out,
-                            bool accumulate, cudaStream_t s);
-// out[i] = sum_s in[s][i] for s in shard order
-void launch_sum_shards(const double* const* in, int nshards, int64_t n, double* out, cudaStream_t s);
+// Canonical SSE (common.cuh canon_*): part[rows][ntiles][2] -> out[rows][2],
+// a function of the multiset of tile partials only.  Single part:
+void launch_reduce_partials(const double* part, int64_t rows, int64_t ntiles, double* out, cudaStream_t s);
+// Several parts (shards, ranks): clear; exp of every part (atomicMax into
+// emax[rows][2]); [allreduce max]; digits of every part (atomicAdd into
+// digits[rows][2][kLimbs]); [allreduce sum]; finish.
+void launch_canon_clear(int64_t rows, int32_t* emax, unsigned long long* digits, cudaStream_t s);
+void launch_canon_exp(const double* part, int64_t rows, int64_t ntiles, int32_t* emax, cudaStream_t s);
+void launch_canon_digits(const double* part, int64_t rows, int64_t ntiles, const int32_t* emax,
+                         unsigned long long* digits, cudaStream_t s);
+void launch_canon_finish(const int32_t* emax, const unsigned long long* digits, int64_t rows, double* sse,
+                         cudaStream_t s);
 
 // fp64 operator RMSE per row of a dense [m][n] matrix (fitness.py:28-51)
 void launch_row_rmse(const double* S, const double* y, int64_t m, int64_t n, double* out,

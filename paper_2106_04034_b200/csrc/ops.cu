@@ -88,38 +88,90 @@ __device__ double block_sum(double v, double* sh) {
   return t;
 }
 
-// part[row][tile][2] -> out[row][2]; tiles are summed per thread in index
-// order, then combined by a fixed tree: a function of case positions only.
-// One warp per row (same order as the fused k_reduce_survive below).
-__global__ void k_reduce_partials(const double* __restrict__ part, int64_t ntiles, int64_t rows,
-                                  double* __restrict__ out) {
-  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (row >= rows) return;
+// Canonical SSE of part[row][tile][2] (common.cuh): one warp per row.  The
+// anchors are the exact max partial exponents; the digit sums are exact.
+__device__ __forceinline__ int2 warp_row_exp(const double* __restrict__ p, int64_t ntiles, int lane) {
+  int32_t ex = kExpZero, ez = kExpZero;
+  for (int64_t t = lane; t < ntiles; t += 32) {
+    const double2 v = *reinterpret_cast<const double2*>(p + 2 * t);
+    ex = max(ex, canon_exp(v.x));
+    ez = max(ez, canon_exp(v.y));
+  }
+  return make_int2(__reduce_max_sync(0xffffffffu, ex), __reduce_max_sync(0xffffffffu, ez));
+}
+
+// per-row digit sums (train L[0..3], test L[4..7]), complete in every lane
+__device__ __forceinline__ void warp_row_digits(const double* __restrict__ p, int64_t ntiles, int lane,
+                                                int2 A, unsigned long long L[2 * kLimbs]) {
+#pragma unroll
+  for (int d = 0; d < 2 * kLimbs; ++d) L[d] = 0;
+  const bool fx = A.x < kExpInf, fz = A.y < kExpInf;
+  for (int64_t t = lane; t < ntiles; t += 32) {
+    const double2 v = *reinterpret_cast<const double2*>(p + 2 * t);
+    if (fx) canon_add(v.x, A.x, L);
+    if (fz) canon_add(v.y, A.y, L + kLimbs);
+  }
+#pragma unroll
+  for (int d = 0; d < 2 * kLimbs; ++d)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) L[d] += __shfl_xor_sync(0xffffffffu, L[d], o);
+}
+
+__device__ __forceinline__ void warp_row_sse(const double* __restrict__ part, int64_t ntiles, int64_t row,
+                                             double* __restrict__ sse) {
   const int lane = threadIdx.x & 31;
   const double* p = part + row * ntiles * 2;
-  double a = 0.0, b = 0.0;
-  for (int64_t t = lane; t < ntiles; t += 32) {
-    a = __dadd_rn(a, p[2 * t]);
-    b = __dadd_rn(b, p[2 * t + 1]);
-  }
-  a = warp_sum(a);
-  b = warp_sum(b);
+  const int2 A = warp_row_exp(p, ntiles, lane);
+  unsigned long long L[2 * kLimbs];
+  warp_row_digits(p, ntiles, lane, A, L);
   if (lane == 0) {
-    out[2 * row] = a;
-    out[2 * row + 1] = b;
+    sse[2 * row] = canon_finish(L, A.x);
+    sse[2 * row + 1] = canon_finish(L + kLimbs, A.y);
   }
 }
 
-struct ShardPtrs {
-  const double* p[16];
-};
+// multi-shard / multi-rank steps: anchors (atomicMax over shards, then an
+// allreduce-max), digits (atomicAdd over shards, then an allreduce-sum), finish
+__global__ void k_reduce_partials(const double* __restrict__ part, int64_t ntiles, int64_t rows,
+                                  double* __restrict__ out) {
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row < rows) warp_row_sse(part, ntiles, row, out);
+}
 
-__global__ void k_sum_shards(ShardPtrs in, int nshards, int64_t n, double* out) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+__global__ void k_canon_exp(const double* __restrict__ part, int64_t ntiles, int64_t rows, int32_t* emax) {
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const int lane = threadIdx.x & 31;
+  const int2 A = warp_row_exp(part + row * ntiles * 2, ntiles, lane);
+  if (lane == 0) {
+    atomicMax(emax + 2 * row, A.x);
+    atomicMax(emax + 2 * row + 1, A.y);
+  }
+}
+
+__global__ void k_canon_digits(const double* __restrict__ part, int64_t ntiles, int64_t rows,
+                               const int32_t* __restrict__ emax, unsigned long long* digits) {
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const int lane = threadIdx.x & 31;
+  unsigned long long L[2 * kLimbs];
+  warp_row_digits(part + row * ntiles * 2, ntiles, lane, make_int2(emax[2 * row], emax[2 * row + 1]), L);
+  if (lane < 2 * kLimbs) {
+    unsigned long long mine = 0;
+#pragma unroll
+    for (int d = 0; d < 2 * kLimbs; ++d) mine = lane == d ? L[d] : mine;
+    if (mine) atomicAdd(digits + row * 2 * kLimbs + lane, mine);
+  }
+}
+
+__global__ void k_canon_finish(const int32_t* __restrict__ emax, const unsigned long long* __restrict__ digits,
+                               int64_t n, double* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;   // (row, train|test)
   if (i >= n) return;
-  double t = in.p[0][i];
-  for (int s = 1; s < nshards; ++s) t = __dadd_rn(t, in.p[s][i]);
-  out[i] = t;
+  unsigned long long L[kLimbs];
+#pragma unroll
+  for (int d = 0; d < kLimbs; ++d) L[d] = digits[(i >> 1) * 2 * kLimbs + (i & 1) * kLimbs + d];
+  out[i] = canon_finish(L, emax[i]);
 }
 
 // fp64 RMSE of each row (operator API, fitness.py:28-51)
@@ -250,28 +302,8 @@ __device__ void survive_block(const SurviveArgs& a) {
 
 __global__ void __launch_bounds__(1024) k_survive(SurviveArgs a) { survive_block(a); }
 
-// SSE tile reduction of every row (one block per row, fixed order) fused
+// Canonical SSE of every row (one warp per row, warp_row_sse above) fused
 // with survival: the last block to finish runs survive_block.
-// One warp per row: lane l sums tiles l, l+32, ... in order, then a fixed
-// butterfly — one wave of blocks, no block barriers on the reduction path.
-__device__ __forceinline__ void warp_row_sse(const double* __restrict__ part, int64_t ntiles,
-                                             int64_t row, double* __restrict__ sse) {
-  const int lane = threadIdx.x & 31;
-  const double* p = part + row * ntiles * 2;
-  double x = 0.0, z = 0.0;
-  for (int64_t t = lane; t < ntiles; t += 32) {
-    const double2 v = *reinterpret_cast<const double2*>(p + 2 * t);
-    x = __dadd_rn(x, v.x);
-    z = __dadd_rn(z, v.y);
-  }
-  x = warp_sum(x);
-  z = warp_sum(z);
-  if (lane == 0) {
-    sse[2 * row] = x;
-    sse[2 * row + 1] = z;
-  }
-}
-
 __global__ void __launch_bounds__(256) k_reduce_survive(const double* __restrict__ part, int64_t ntiles,
                                                         double* __restrict__ sse, SurviveArgs a,
                                                         unsigned int* done) {
@@ -388,19 +420,34 @@ void launch_plan(const PlanParams& p, int64_t gen, const int64_t* gen_ptr, int64
   check_launch();
 }
 
-void launch_reduce_partials(const double* part, int64_t rows, int64_t ntiles, double* out,
-                            bool accumulate, cudaStream_t s) {
-  if (rows <= 0) return;
-  GSGP_REQUIRE(!accumulate, "accumulating partial reduction is not supported");
-  k_reduce_partials<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(part, ntiles, rows, out);
+void launch_canon_clear(int64_t rows, int32_t* emax, unsigned long long* digits, cudaStream_t s) {
+  GSGP_CUDA(cudaMemsetAsync(emax, 0x80, rows * 2 * 4, s));   // 0x80808080 == kExpZero
+  GSGP_CUDA(cudaMemsetAsync(digits, 0, rows * 2 * kLimbs * 8, s));
+}
+
+void launch_canon_exp(const double* part, int64_t rows, int64_t ntiles, int32_t* emax, cudaStream_t s) {
+  if (rows <= 0 || ntiles <= 0) return;
+  k_canon_exp<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(part, ntiles, rows, emax);
   check_launch();
 }
 
-void launch_sum_shards(const double* const* in, int nshards, int64_t n, double* out, cudaStream_t s) {
-  GSGP_REQUIRE(nshards >= 1 && nshards <= 16, "1..16 local shards supported");
-  ShardPtrs sp{};
-  for (int i = 0; i < nshards; ++i) sp.p[i] = in[i];
-  k_sum_shards<<<blocks_for(n), kThreads, 0, s>>>(sp, nshards, n, out);
+void launch_canon_digits(const double* part, int64_t rows, int64_t ntiles, const int32_t* emax,
+                         unsigned long long* digits, cudaStream_t s) {
+  if (rows <= 0 || ntiles <= 0) return;
+  k_canon_digits<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(part, ntiles, rows, emax, digits);
+  check_launch();
+}
+
+void launch_canon_finish(const int32_t* emax, const unsigned long long* digits, int64_t rows, double* sse,
+                         cudaStream_t s) {
+  if (rows <= 0) return;
+  k_canon_finish<<<blocks_for(rows * 2), kThreads, 0, s>>>(emax, digits, rows * 2, sse);
+  check_launch();
+}
+
+void launch_reduce_partials(const double* part, int64_t rows, int64_t ntiles, double* out, cudaStream_t s) {
+  if (rows <= 0) return;
+  k_reduce_partials<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(part, ntiles, rows, out);
   check_launch();
 }
 

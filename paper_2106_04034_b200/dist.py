@@ -4,9 +4,12 @@
 libgsgp_b200.so, it is broadcast over the existing process group, and every
 rank joins the library's own NCCL communicator (`gsgp_comm_init`).  After
 that `run_evolution` shards the train and test cases contiguously across
-ranks and the only per-generation collective is an NCCL allreduce of the
-[m][2] partial-SSE vector; genomes, plans and every survival
-decision are recomputed identically on each rank from the counter RNG.
+ranks (slices aligned to CASE_ALIGN cases) and the per-generation collectives
+are two small NCCL allreduces of the canonical SSE — the rows' partial
+exponent anchors (max) and their exact fixed-point digit sums (sum) — so the
+SSE, and every decision, is bit-identical for any number of ranks (SURVEY
+§8e); genomes, plans and survival are recomputed identically on each rank
+from the counter RNG.
 """
 
 from __future__ import annotations
@@ -19,10 +22,18 @@ from . import _lib
 from ._lib import check
 
 
-def shard_range(n: int, count: int, index: int) -> tuple[int, int]:
+CASE_ALIGN = 12288
+"""Shard boundaries are multiples of this many cases (engine.cu kCaseAlign:
+the lcm of every SSE tile), which keeps the SSE tile partials — and with the
+canonical sum the whole run — identical for any number of shards."""
+
+
+def shard_range(n: int, count: int, index: int, align: int = CASE_ALIGN) -> tuple[int, int]:
     """Contiguous slice [lo, hi) of shard `index` out of `count` (same
-    formula as gsgp_shard_range in engine.cu)."""
-    return (n * index) // count, (n * (index + 1)) // count
+    formula as gsgp_shard_range in engine.cu for the default `align`)."""
+    def cut(i):
+        return n if i >= count else (n * i) // count // align * align
+    return cut(index), cut(index + 1)
 
 
 def init_from_torch(group=None) -> tuple[int, int]:
@@ -54,15 +65,19 @@ def init_host_exchange(group=None) -> tuple[int, int]:
     import torch.distributed as td
     global _host_cb
     world, rank = td.get_world_size(group), td.get_rank(group)
-    dtypes = {0: (np.float64, 8), 1: (np.int32, 4), 2: (np.uint64, 8)}
+    # engine.cu HostRed: 0 fp64 sum, 1 int32 sum, 2 uint64 sum, 3 int32 max
+    kinds = {0: (np.float64, 8, td.ReduceOp.SUM), 1: (np.int32, 4, td.ReduceOp.SUM),
+             2: (np.uint64, 8, td.ReduceOp.SUM), 3: (np.int32, 4, td.ReduceOp.MAX)}
 
-    def allreduce(ptr, count, dtype):
-        npt, esz = dtypes[int(dtype)]
+    def allreduce(ptr, count, kind):
+        npt, esz, op = kinds[int(kind)]
         buf = np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_ubyte)), shape=(count * esz,))
         arr = buf.view(npt)
-        t = torch.from_numpy(arr.astype(np.int64) if npt is np.uint64 else arr.copy())
-        td.all_reduce(t, op=td.ReduceOp.SUM, group=group)
-        arr[:] = t.numpy().astype(npt)
+        # uint64 digit sums travel as int64: two's-complement addition is the
+        # same bits (the sums stay far below 2^63)
+        t = torch.from_numpy(arr.view(np.int64).copy() if npt is np.uint64 else arr.copy())
+        td.all_reduce(t, op=op, group=group)
+        arr[:] = t.numpy().view(npt) if npt is np.uint64 else t.numpy()
 
     _host_cb = HOST_ALLREDUCE(allreduce)
     check(_lib.load().gsgp_comm_init_host(world, rank, C.cast(_host_cb, C.c_void_p)))

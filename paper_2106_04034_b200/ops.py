@@ -204,6 +204,20 @@ def sigmoid_array(x: np.ndarray) -> np.ndarray:
     return out
 
 
+def canonical_sum(x: np.ndarray, parts: int = 0) -> np.ndarray:
+    """Row sums of non-negative fp64 values with the engine's canonical SSE
+    reduction (csrc/common.cuh): exact fixed-point digit sums anchored on the
+    row's largest exponent, rounded once — independent of the order and
+    grouping of the values.  `parts` > 0 runs the multi-shard path over that
+    many column pieces (same bits as the fused path by construction)."""
+    a = np.ascontiguousarray(np.atleast_2d(np.asarray(x, dtype=np.float64)))
+    if a.size == 0:
+        raise ConfigError("canonical_sum needs a non-empty matrix")
+    out = np.empty(a.shape[0])
+    check(_lib.load().gsgp_canonical_sum(ptr(a.reshape(-1)), a.shape[0], a.shape[1], int(parts), ptr(out)))
+    return out
+
+
 def sigmoid(x: float) -> float:
     """gsgp/mutation.py:26-29."""
     return float(sigmoid_array(np.array([float(x)]))[0])

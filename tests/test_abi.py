@@ -57,11 +57,15 @@ def test_shard_ranges_partition_the_cases():
     import ctypes as C
     from paper_2106_04034_b200 import _lib, dist
     lib = _lib.load()
-    for n in (1, 7, 100, 12_500_000):
+    for n in (1, 7, 100, 12_287, 12_288, 50_000, 12_500_000):
         for count in (1, 2, 3, 8):
             spans = [dist.shard_range(n, count, i) for i in range(count)]
             assert spans[0][0] == 0 and spans[-1][1] == n
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+            # interior boundaries sit on the canonical case grid, and the
+            # split stays balanced to within one alignment block
+            assert all(hi % dist.CASE_ALIGN == 0 for _, hi in spans[:-1])
+            assert all(hi - lo <= -(-n // count) + dist.CASE_ALIGN for lo, hi in spans)
             for i, (lo, hi) in enumerate(spans):
                 clo, chi = C.c_int64(), C.c_int64()
                 lib.gsgp_shard_range(n, count, i, C.byref(clo), C.byref(chi))

@@ -3,9 +3,11 @@ SURVEY §8e) with 2 and 3 real processes sharing this GPU: the collectives
 go through `dist.init_host_exchange` (host memory + gloo) instead of NCCL —
 same partition, same exchanged values, same decision logic in the library.
 Every rank must return the single-process run's elite trace and traces
-(bit-identical: the exchanged SSE partial sums only change the summation
-grouping) and the reference's golden elite trace; the gathered elite
-semantics must equal the single-process elite semantics."""
+bit for bit (the canonical SSE does not depend on the split) and the
+reference's golden elite trace; the gathered elite semantics must equal the
+single-process elite semantics.  The goldens are smaller than one 12288-case
+shard block, so here the leading ranks hold empty slices; real splits of
+large datasets are in test_gpu_canonical.py."""
 
 from __future__ import annotations
 
@@ -73,8 +75,7 @@ def test_ranks_sharing_a_gpu_reproduce_single_process_run(name, world, vshards):
     assert one_elite == ref_elite
     for rank, elite, train, test, overflow, full in got:
         assert elite == one_elite, rank
-        np.testing.assert_allclose(train, one.train_fitness, rtol=1e-12, atol=0)
-        np.testing.assert_allclose(test, one.test_fitness, rtol=1e-12, atol=0)
+        assert train == one.train_fitness.tolist() and test == one.test_fitness.tolist()
         assert overflow == one.overflow_replacements
         assert np.array_equal(np.array(full), one.elite_train_semantics)
     assert all(r[2] == got[0][2] and r[3] == got[0][3] for r in got)   # identical on every rank
@@ -177,5 +178,5 @@ def test_random_configs_across_ranks(seed, world, vshards, tiny):
     one_elite = [(e.elite.source, e.elite.index, e.elite.slot) for e in one.lineage.entries]
     for rank, elite, train, full in got:
         assert elite == one_elite, (rank, kw)
-        np.testing.assert_allclose(train, one.train_fitness, rtol=1e-12, atol=0)
+        assert train == one.train_fitness.tolist(), (rank, kw)
         assert np.array_equal(np.array(full), one.elite_train_semantics)
