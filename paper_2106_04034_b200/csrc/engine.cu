@@ -674,6 +674,11 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   done.alloc(16);
   GSGP_CUDA(cudaMemsetAsync(done.p, 0, 16, st));
   const bool fused_tail = (G == 1 && W == 1);
+  // fused tail: the GSM launch accumulates the canonical-sum anchors, the
+  // reduce reads the partials once and re-arms the anchors (kExpZero)
+  DevBuf gemax;
+  gemax.alloc(m * 2 * 4);
+  GSGP_CUDA(cudaMemsetAsync(gemax.p, 0x80, m * 2 * 4, st));
   // one generation: GSM+SSE with the plan drawn inline (per shard), then the
   // canonical SSE and survival — fused into one kernel when there is a
   // single shard, else anchors / digits per shard -> allreduce -> finish -> survive
@@ -700,6 +705,7 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
       a.sign = cfg->gsm_sign;
       a.part = p->part.as<double>();
       a.ticket = p->ticket.as<unsigned long long>();
+      a.emax = fused_tail ? gemax.as<int32_t>() : nullptr;
       a.plan_inline = 1;
       a.write_plan = plan_written ? 0 : 1;   // the first non-empty shard records the plan
       plan_written = true;
@@ -713,7 +719,8 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
     }
     if (t1) GSGP_CUDA(cudaEventRecord(t1->e, s));
     if (fused_tail) {
-      launch_reduce_survive(sh[0]->part.as<double>(), sh[0]->ntiles, sse_vec, sa, done.as<unsigned int>(), s);
+      launch_reduce_survive(sh[0]->part.as<double>(), sh[0]->ntiles, gemax.as<int32_t>(), sse_vec, sa,
+                            done.as<unsigned int>(), s);
       ++n;
     } else {
       canon_sse(false, sse_vec, s);

@@ -119,6 +119,8 @@ struct GsmArgs {
   const int64_t* ctl;       // device control block (see engine.cu), may be nullptr
   int32_t sign;             // 0 minus, 1 plus
   double* part;             // [m][gsm_tiles][2]
+  int32_t* emax;            // optional [m][2]: atomicMax of the partials' canon_exp (fused tail);
+                            // must hold kExpZero before the launch (the reduce resets it)
   unsigned long long* nonfinite;   // operator mode only
   // {ticket, exited CTAs}: dynamic unit dispatch; zero before the first
   // launch, the last CTA to exit re-zeroes both for the next launch
@@ -130,10 +132,10 @@ struct GsmArgs {
   int32_t write_plan;
   PlanParams plan;
 };
-// case tiles of a row: train tiles over [0, test_off), then test tiles over
-// [test_off, pitch) (the part[] row stride); cases per tile
+// units per row (the part[] row stride): train tiles over [0, test_off),
+// then test tiles over [test_off, pitch), the two partial tails merged into
+// one unit when they fit (gsm.cu unit_span); cases per tile
 int64_t gsm_tiles(int64_t pitch, int64_t test_off, bool f64);
-int64_t gsm_train_tiles(int64_t test_off, bool f64);
 int64_t gsm_tile_cases(bool f64);
 void launch_gsm(const GsmArgs& a, bool f64, bool operator_mode, cudaStream_t s);
 // SSE of the stored semantics S against y in the generation kernel's exact
@@ -175,10 +177,11 @@ struct SurviveArgs {
   double* trace_tr; double* trace_te;
 };
 void launch_survive(const SurviveArgs& a, cudaStream_t s);
-// per-row SSE tile reduction into sse (== a.sse_off) fused with survival
-// (single shard, single rank); `done` is a zeroed counter, re-zeroed on exit
-void launch_reduce_survive(const double* part, int64_t ntiles, double* sse, const SurviveArgs& a,
-                           unsigned int* done, cudaStream_t s);
+// per-row canonical SSE into sse (== a.sse_off) fused with survival (single
+// shard, single rank); emax = the anchors the GSM launch accumulated (reset
+// to kExpZero here); `done` is a zeroed counter, re-zeroed on exit
+void launch_reduce_survive(const double* part, int64_t ntiles, int32_t* emax, double* sse,
+                           const SurviveArgs& a, unsigned int* done, cudaStream_t s);
 // initial elite: fitness from SSE, argmin, trace[0] (evolution.py:132-143)
 void launch_init_state(const SurviveArgs& a, cudaStream_t s);
 // decision only, for the operator API: out = {src, idx, slot}

@@ -130,6 +130,67 @@ __device__ __forceinline__ void warp_row_sse(const double* __restrict__ part, in
   }
 }
 
+// the fused generation tail: anchors come from the GSM launch (emax), which
+// is reset to kExpZero for the next generation once read
+__device__ __forceinline__ void warp_row_sse_anchored(const double* __restrict__ part, int64_t ntiles,
+                                                      int64_t row, int32_t* emax, double* __restrict__ sse) {
+  const int lane = threadIdx.x & 31;
+  int2 A = make_int2(0, 0);
+  if (lane == 0) {
+    A = *reinterpret_cast<int2*>(emax + 2 * row);
+    *reinterpret_cast<int2*>(emax + 2 * row) = make_int2(kExpZero, kExpZero);
+  }
+  A.x = __shfl_sync(0xffffffffu, A.x, 0);
+  A.y = __shfl_sync(0xffffffffu, A.y, 0);
+  unsigned long long L[2 * kLimbs];
+  warp_row_digits(part + row * ntiles * 2, ntiles, lane, A, L);
+  if (lane == 0) {
+    sse[2 * row] = canon_finish(L, A.x);
+    sse[2 * row + 1] = canon_finish(L + kLimbs, A.y);
+  }
+}
+
+// one 256-thread block per row, for long rows (C3: ~3000 tiles): the same
+// anchors and exact digit sums as warp_row_sse, 8x the loads in flight
+__device__ void block_row_sse(const double* __restrict__ part, int64_t ntiles, int64_t row,
+                              int32_t* emax, double* __restrict__ sse) {
+  __shared__ int2 sh_a;
+  __shared__ unsigned long long sh_d[8][2 * kLimbs];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const double* p = part + row * ntiles * 2;
+  if (tid == 0) {
+    sh_a = *reinterpret_cast<int2*>(emax + 2 * row);
+    *reinterpret_cast<int2*>(emax + 2 * row) = make_int2(kExpZero, kExpZero);
+  }
+  __syncthreads();
+  const int2 A = sh_a;
+  unsigned long long L[2 * kLimbs];
+#pragma unroll
+  for (int d = 0; d < 2 * kLimbs; ++d) L[d] = 0;
+  const bool fx = A.x < kExpInf, fz = A.y < kExpInf;
+  for (int64_t t = tid; t < ntiles; t += 256) {
+    const double2 v = *reinterpret_cast<const double2*>(p + 2 * t);
+    if (fx) canon_add(v.x, A.x, L);
+    if (fz) canon_add(v.y, A.y, L + kLimbs);
+  }
+#pragma unroll
+  for (int d = 0; d < 2 * kLimbs; ++d) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) L[d] += __shfl_xor_sync(0xffffffffu, L[d], o);
+    if (lane == 0) sh_d[w][d] = L[d];
+  }
+  __syncthreads();
+  if (tid < 2) {
+    unsigned long long T[kLimbs];
+#pragma unroll
+    for (int d = 0; d < kLimbs; ++d) {
+      T[d] = 0;
+      for (int i = 0; i < 8; ++i) T[d] += sh_d[i][tid * kLimbs + d];
+    }
+    sse[2 * row + tid] = canon_finish(T, tid ? A.y : A.x);
+  }
+}
+
 // multi-shard / multi-rank steps: anchors (atomicMax over shards, then an
 // allreduce-max), digits (atomicAdd over shards, then an allreduce-sum), finish
 __global__ void k_reduce_partials(const double* __restrict__ part, int64_t ntiles, int64_t rows,
@@ -305,11 +366,26 @@ __global__ void __launch_bounds__(1024) k_survive(SurviveArgs a) { survive_block
 // Canonical SSE of every row (one warp per row, warp_row_sse above) fused
 // with survival: the last block to finish runs survive_block.
 __global__ void __launch_bounds__(256) k_reduce_survive(const double* __restrict__ part, int64_t ntiles,
-                                                        double* __restrict__ sse, SurviveArgs a,
-                                                        unsigned int* done) {
+                                                        int32_t* emax, double* __restrict__ sse,
+                                                        SurviveArgs a, unsigned int* done) {
   __shared__ int last;
   const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (row < a.m) warp_row_sse(part, ntiles, row, sse);
+  if (row < a.m) warp_row_sse_anchored(part, ntiles, row, emax, sse);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  survive_block(a);
+  if (threadIdx.x == 0) *done = 0;
+}
+
+__global__ void __launch_bounds__(256) k_reduce_survive_wide(const double* __restrict__ part, int64_t ntiles,
+                                                             int32_t* emax, double* __restrict__ sse,
+                                                             SurviveArgs a, unsigned int* done) {
+  __shared__ int last;
+  block_row_sse(part, ntiles, blockIdx.x, emax, sse);
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
@@ -458,9 +534,12 @@ void launch_row_rmse(const double* S, const double* y, int64_t m, int64_t n, dou
   check_launch();
 }
 
-void launch_reduce_survive(const double* part, int64_t ntiles, double* sse, const SurviveArgs& a,
-                           unsigned int* done, cudaStream_t s) {
-  k_reduce_survive<<<(unsigned)((a.m + 7) / 8), 256, 0, s>>>(part, ntiles, sse, a, done);
+void launch_reduce_survive(const double* part, int64_t ntiles, int32_t* emax, double* sse,
+                           const SurviveArgs& a, unsigned int* done, cudaStream_t s) {
+  if (ntiles >= 256)   // long rows (C3 ~3000 tiles): a block per row
+    k_reduce_survive_wide<<<(unsigned)a.m, 256, 0, s>>>(part, ntiles, emax, sse, a, done);
+  else
+    k_reduce_survive<<<(unsigned)((a.m + 7) / 8), 256, 0, s>>>(part, ntiles, emax, sse, a, done);
   check_launch();
 }
 
