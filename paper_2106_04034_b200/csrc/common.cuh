@@ -218,11 +218,12 @@ __device__ __forceinline__ double canon_finish(const unsigned long long L[kLimbs
   if (lo <= 0) {
     top = w0 << (-lo);
   } else {
-    const int q = lo >> 6, r = lo & 63;
-    const uint64_t w[4] = {w0, w1, w2, 0};
-    top = r ? (w[q] >> r) | (w[q + 1] << (64 - r)) : w[q];
-    for (int i = 0; i < q; ++i) below |= w[i] != 0;
-    if (r) below |= (w[q] & ((1ull << r) - 1)) != 0;
+    const int q = lo >> 6, r = lo & 63;   // q in {0, 1, 2}
+    const uint64_t wq = q == 0 ? w0 : (q == 1 ? w1 : w2);
+    const uint64_t wn = q == 0 ? w1 : (q == 1 ? w2 : 0ull);
+    top = r ? (wq >> r) | (wn << (64 - r)) : wq;
+    below = (q >= 1 && w0 != 0) || (q >= 2 && w1 != 0);
+    if (r) below |= (wq & ((1ull << r) - 1)) != 0;
   }
   uint64_t mant = top >> 11;
   const bool rnd = (top >> 10) & 1;

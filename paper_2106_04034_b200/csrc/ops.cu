@@ -135,19 +135,33 @@ __device__ __forceinline__ void warp_row_sse(const double* __restrict__ part, in
 __device__ __forceinline__ void warp_row_sse_anchored(const double* __restrict__ part, int64_t ntiles,
                                                       int64_t row, int32_t* emax, double* __restrict__ sse) {
   const int lane = threadIdx.x & 31;
-  int2 A = make_int2(0, 0);
-  if (lane == 0) {
-    A = *reinterpret_cast<int2*>(emax + 2 * row);
-    *reinterpret_cast<int2*>(emax + 2 * row) = make_int2(kExpZero, kExpZero);
+  const double* p = part + row * ntiles * 2;
+  // short rows (the launcher sends rows of < 256 units here): every lane
+  // issues its partial loads before the anchor load, so the latencies overlap
+  constexpr int kPer = 8;
+  double2 v[kPer];
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const int64_t t = lane + 32 * j;
+    v[j] = t < ntiles ? *reinterpret_cast<const double2*>(p + 2 * t) : make_double2(0.0, 0.0);
   }
-  A.x = __shfl_sync(0xffffffffu, A.x, 0);
-  A.y = __shfl_sync(0xffffffffu, A.y, 0);
+  const int2 A = *reinterpret_cast<const int2*>(emax + 2 * row);
+  __syncwarp();
+  if (lane == 0) *reinterpret_cast<int2*>(emax + 2 * row) = make_int2(kExpZero, kExpZero);
   unsigned long long L[2 * kLimbs];
-  warp_row_digits(part + row * ntiles * 2, ntiles, lane, A, L);
-  if (lane == 0) {
-    sse[2 * row] = canon_finish(L, A.x);
-    sse[2 * row + 1] = canon_finish(L + kLimbs, A.y);
+#pragma unroll
+  for (int d = 0; d < 2 * kLimbs; ++d) L[d] = 0;
+  const bool fx = A.x < kExpInf, fz = A.y < kExpInf;
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    if (fx) canon_add(v[j].x, A.x, L);
+    if (fz) canon_add(v[j].y, A.y, L + kLimbs);
   }
+#pragma unroll
+  for (int d = 0; d < 2 * kLimbs; ++d)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) L[d] += __shfl_xor_sync(0xffffffffu, L[d], o);
+  if (lane < 2) sse[2 * row + lane] = canon_finish(lane ? L + kLimbs : L, lane ? A.y : A.x);   // train | test
 }
 
 // one 256-thread block per row, for long rows (C3: ~3000 tiles): the same
@@ -158,6 +172,18 @@ __device__ void block_row_sse(const double* __restrict__ part, int64_t ntiles, i
   __shared__ unsigned long long sh_d[8][2 * kLimbs];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const double* p = part + row * ntiles * 2;
+  // groups of 4 strided loads in flight per thread; the first group is
+  // issued before the anchor handshake
+  constexpr int kGrp = 4;
+  auto load = [&](int64_t t0, double2* v) {
+#pragma unroll
+    for (int j = 0; j < kGrp; ++j) {
+      const int64_t t = t0 + 256 * j;
+      v[j] = t < ntiles ? *reinterpret_cast<const double2*>(p + 2 * t) : make_double2(0.0, 0.0);
+    }
+  };
+  double2 v[kGrp];
+  load(tid, v);
   if (tid == 0) {
     sh_a = *reinterpret_cast<int2*>(emax + 2 * row);
     *reinterpret_cast<int2*>(emax + 2 * row) = make_int2(kExpZero, kExpZero);
@@ -168,10 +194,15 @@ __device__ void block_row_sse(const double* __restrict__ part, int64_t ntiles, i
 #pragma unroll
   for (int d = 0; d < 2 * kLimbs; ++d) L[d] = 0;
   const bool fx = A.x < kExpInf, fz = A.y < kExpInf;
-  for (int64_t t = tid; t < ntiles; t += 256) {
-    const double2 v = *reinterpret_cast<const double2*>(p + 2 * t);
-    if (fx) canon_add(v.x, A.x, L);
-    if (fz) canon_add(v.y, A.y, L + kLimbs);
+  for (int64_t t0 = tid;;) {
+#pragma unroll
+    for (int j = 0; j < kGrp; ++j) {
+      if (fx) canon_add(v[j].x, A.x, L);
+      if (fz) canon_add(v[j].y, A.y, L + kLimbs);
+    }
+    t0 += 256 * kGrp;
+    if (t0 - tid >= ntiles) break;
+    load(t0, v);
   }
 #pragma unroll
   for (int d = 0; d < 2 * kLimbs; ++d) {
@@ -536,7 +567,7 @@ void launch_row_rmse(const double* S, const double* y, int64_t m, int64_t n, dou
 
 void launch_reduce_survive(const double* part, int64_t ntiles, int32_t* emax, double* sse,
                            const SurviveArgs& a, unsigned int* done, cudaStream_t s) {
-  if (ntiles >= 256)   // long rows (C3 ~3000 tiles): a block per row
+  if (ntiles > 256)    // long rows (C3 ~3000 tiles): a block per row; else a warp (8 loads per lane)
     k_reduce_survive_wide<<<(unsigned)a.m, 256, 0, s>>>(part, ntiles, emax, sse, a, done);
   else
     k_reduce_survive<<<(unsigned)((a.m + 7) / 8), 256, 0, s>>>(part, ntiles, emax, sse, a, done);
