@@ -294,7 +294,8 @@ int gsgp_gsm(const double* parent, int64_t m, int64_t n, const double* trees, in
     h2d(du.p, u, m * 8);
     h2d(dv.p, v, m * 8);
     h2d(dm.p, ms, m * 8);
-    const int64_t ntiles = gsm_tiles(pitch, pitch, true);
+    const RowLayout lay = make_layout(n, 0, true);   // [train] = pad32(n) == pitch
+    const int64_t ntiles = lay.ntiles;
     Buf part(m * ntiles * 2 * 8);
     GsmArgs a{};
     a.pool = T.p;
@@ -302,8 +303,7 @@ int gsgp_gsm(const double* parent, int64_t m, int64_t n, const double* trees, in
     a.elite_prev = e0.p;
     a.elite_cur = e1.p;
     a.y = y.as<double>();
-    a.pitch = pitch;
-    a.test_off = pitch;
+    a.lay = lay;
     a.m = m;
     a.u = du.as<int64_t>();
     a.v = dv.as<int64_t>();
@@ -352,7 +352,8 @@ int gsgp_gsm_step_f32(const float* parent_tr, const float* parent_te, const floa
     h2d(du.p, u, m * 8);
     h2d(dv.p, v, m * 8);
     h2d(dm.p, ms, m * 8);
-    const int64_t ntiles = gsm_tiles(pitch, toff, false);
+    const RowLayout lay = make_layout(ntr, nte, false, false);   // [train | test], as staged above
+    const int64_t ntiles = lay.ntiles;
     Buf part(m * ntiles * 2 * 8);
     GsmArgs a{};
     a.pool = T.p;
@@ -360,8 +361,7 @@ int gsgp_gsm_step_f32(const float* parent_tr, const float* parent_te, const floa
     a.elite_prev = e0.p;
     a.elite_cur = e1.p;
     a.y = y.as<double>();
-    a.pitch = pitch;
-    a.test_off = toff;
+    a.lay = lay;
     a.m = m;
     a.u = du.as<int64_t>();
     a.v = dv.as<int64_t>();

@@ -312,7 +312,8 @@ void trim_device_memory() {
 
 struct Shard {
   int64_t tr_lo = 0, tr_hi = 0, te_lo = 0, te_hi = 0;
-  int64_t ntr = 0, nte = 0, pitch = 0, test_off = 0, ntiles = 0, itiles = 0;
+  int64_t ntr = 0, nte = 0, pitch = 0, ntiles = 0, itiles = 0;
+  RowLayout lay{};
   DevBuf S, pool, elite[2], y_store, part, ipart, ticket;
 };
 
@@ -366,9 +367,9 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
     shard_range(nte, nsh_total, gs, &p->te_lo, &p->te_hi);
     p->ntr = p->tr_hi - p->tr_lo;
     p->nte = p->te_hi - p->te_lo;
-    p->test_off = pad32(p->ntr);
-    p->pitch = p->test_off + pad32(p->nte);
-    p->ntiles = gsm_tiles(p->pitch, p->test_off, f64);
+    p->lay = make_layout(p->ntr, p->nte, f64);
+    p->pitch = p->lay.pitch;
+    p->ntiles = p->lay.ntiles;
     sh.push_back(std::move(p));
   }
   out->shard_train_lo = sh.front()->tr_lo;
@@ -479,7 +480,9 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
     ia.out = p->S.p;
     ia.out_is_f64 = f64 ? 1 : 0;
     ia.pitch = p->pitch;
-    ia.test_off = p->test_off;
+    ia.test_off = p->lay.test_off;
+    ia.te_full = p->lay.te_full;
+    ia.tail_off = p->lay.tail_off;
     ia.y = p->y_store.as<double>();
     ia.wide = wide.as<int32_t>();
     ia.nonfinite = nonfinite.as<unsigned long long>();
@@ -550,9 +553,17 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
       GSGP_CUDA(cudaMemcpyAsync(Xr[b].p, hx, nq * l * 8, cudaMemcpyHostToDevice, up));
       if (ntr_part > 0)
         GSGP_CUDA(cudaMemcpyAsync(p->y_store.as<double>() + c0, hy, ntr_part * 8, cudaMemcpyHostToDevice, up));
-      if (nte_part > 0)
-        GSGP_CUDA(cudaMemcpyAsync(p->y_store.as<double>() + p->test_off + (te_beg - ia.te_q),
-                                  hy + (te_beg - c0), nte_part * 8, cudaMemcpyHostToDevice, up));
+      if (nte_part > 0) {   // test targets [j0, j0 + nte_part) in storage order (RowLayout)
+        const int64_t j0 = te_beg - ia.te_q;
+        const int64_t nfull = std::max<int64_t>(0, std::min(j0 + nte_part, p->lay.te_full) - j0);
+        const double* src = hy + (te_beg - c0);
+        if (nfull > 0)
+          GSGP_CUDA(cudaMemcpyAsync(p->y_store.as<double>() + test_col(p->lay, j0), src, nfull * 8,
+                                    cudaMemcpyHostToDevice, up));
+        if (nte_part > nfull)
+          GSGP_CUDA(cudaMemcpyAsync(p->y_store.as<double>() + test_col(p->lay, j0 + nfull), src + nfull,
+                                    (nte_part - nfull) * 8, cudaMemcpyHostToDevice, up));
+      }
       GSGP_CUDA(cudaEventRecord(ev_h2d[b].e, up));
       GSGP_CUDA(cudaStreamWaitEvent(st, ev_h2d[b].e, 0));
       k_transpose<<<nblk(nq * l), 256, 0, st>>>(Xr[b].as<double>(), nq, l, XT[b].as<double>());
@@ -583,8 +594,7 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
     ga.elite_prev = p->elite[0].p;
     ga.elite_cur = p->elite[1].p;
     ga.y = p->y_store.as<double>();
-    ga.pitch = p->pitch;
-    ga.test_off = p->test_off;
+    ga.lay = p->lay;
     ga.m = m;
     ga.part = p->part.as<double>();
     ga.ticket = p->ticket.as<unsigned long long>();
@@ -695,8 +705,7 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
       a.elite_prev = p->elite[0].p;
       a.elite_cur = p->elite[1].p;
       a.y = p->y_store.as<double>();
-      a.pitch = p->pitch;
-      a.test_off = p->test_off;
+      a.lay = p->lay;
       a.m = m;
       a.u = pu.as<int64_t>();
       a.v = pv.as<int64_t>();

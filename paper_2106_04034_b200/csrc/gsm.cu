@@ -42,33 +42,32 @@ __device__ __forceinline__ double mut(double p, double a, double b, double ms, i
   return __dadd_rn(p, __dmul_rn(t, ms));
 }
 
-// Case tiles are anchored separately on the train region [0, test_off) and
-// the test region [test_off, pitch): tiles 0 .. ttr-1 cover train, the rest
-// test, so no tile straddles the two and — with shard slices starting on
-// multiples of kCaseAlign (engine.cu) — every tile holds the same global
-// cases at the same positions for any shard/rank split (canonical partials).
-// When the partial train tail and the partial test tail fit in one tile
-// together (`merge`), they travel as ONE unit (tile ttr-1): segment A = the
-// train tail, segment B = the test tail, staged back to back.  Both tails
-// always sit on the last shard, with the same lengths, so the merged unit is
-// canonical too; it keeps the unit count of a pitch-wide tiling (each unit
-// costs a fixed pipeline round trip: +3 % units measured +2 % time at C2).
+// Units follow the shard's RowLayout (kernels.cuh): tiles anchored on the
+// train region and on the test region separately, so no plain tile mixes
+// train and test cases and — with shard slices on the kCaseAlign grid
+// (engine.cu) — every tile holds the same global cases at the same positions
+// for any shard/rank split (canonical partials).  When the two partial tails
+// fit in one tile, the layout stores the test tail right after the train
+// region, so the train tail + test tail are ONE contiguous unit whose first
+// nA elements are train: the unit count of a pitch-wide tiling is kept
+// (each unit costs a fixed pipeline round trip; +3 % units measured +2 % time
+// at C2) and every unit is a single span.
 struct UnitSpan {
-  int64_t offA, offB;   // storage offsets of segment A and B (B: merged test tail)
-  int32_t nA, nB;       // elements (nB = 0: a plain tile)
+  int64_t off;   // storage offset
+  int32_t n;     // elements
+  int32_t nA;    // the first nA elements are train cases, the rest test
 };
-__device__ __forceinline__ UnitSpan unit_span(int64_t t, int64_t ttr, int64_t tte, int merge, int64_t tile,
-                                              int64_t test_off, int64_t pitch) {
+__device__ __forceinline__ UnitSpan unit_span(int64_t t, const RowLayout& L) {
   UnitSpan u;
-  const int64_t o = t < ttr ? t * tile : test_off + (t - ttr) * tile;
-  const int64_t end = t < ttr ? test_off : pitch;
-  u.offA = o;
-  u.nA = (int32_t)min(tile, end - o);
-  u.offB = 0;
-  u.nB = 0;
-  if (merge && t == ttr - 1) {
-    u.offB = test_off + (tte - 1) * tile;
-    u.nB = (int32_t)(pitch - u.offB);
+  if (t < L.ttr) {
+    u.off = t * L.tile;
+    const int64_t end = (t == L.ttr - 1 && L.tail_off >= 0) ? L.tail_off + L.tail_pad : L.ntr_pad;
+    u.n = (int32_t)min(L.tile, end - u.off);
+    u.nA = (int32_t)min((int64_t)u.n, L.ntr_pad - u.off);
+  } else {
+    u.off = L.test_off + (t - L.ttr) * L.tile;
+    u.n = (int32_t)min(L.tile, L.pitch - u.off);
+    u.nA = 0;
   }
   return u;
 }
@@ -169,7 +168,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // offspring that equals its parent bit for bit ties with it, as in numpy).
 template <typename T, bool kOp, bool kSseOnly = false>
 __global__ void __launch_bounds__(kTmaThreads, 1)
-k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t ttr, int64_t tte, int merge, int64_t nunits, int kBatch) {
+k_gsm_tma(GsmArgs a, int64_t nunits, int kBatch) {
   using Vec = typename Vec16<T>::type;
   constexpr int EV = Vec16<T>::n;
   constexpr int TILE = kTileBytes / (int)sizeof(T);   // elements per unit
@@ -185,8 +184,8 @@ k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t ttr, int64_t tte, int merge, int64_
   int64_t* slot_unit = reinterpret_cast<int64_t*>(rempty + kRedStages);   // [S] unit in stage
   int64_t* red_unit = slot_unit + kStages;                                // [RS] unit in red slot
   double* slot_ms = reinterpret_cast<double*>(red_unit + kRedStages);     // [S] mutation step
-  int4* slot_it = reinterpret_cast<int4*>(slot_ms + kStages);             // [S] (row i, tile t, nA, nB)
-  longlong2* slot_off = reinterpret_cast<longlong2*>(slot_it + kStages);  // [S] (offA, offB)
+  int4* slot_it = reinterpret_cast<int4*>(slot_ms + kStages);             // [S] (row i, tile t, n, nA)
+  int64_t* slot_off = reinterpret_cast<int64_t*>(slot_it + kStages);      // [S] storage offset of the unit
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t m = a.m;
@@ -265,7 +264,7 @@ k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t ttr, int64_t tte, int merge, int64_
       // lane 0's per-unit path below is shuffles, slot writes and copies only
       const int64_t ub_unit = base + lane;
       int64_t tb = 0, ib = 0, ub = 0, vb = 0;
-      UnitSpan sp{0, 0, 0, 0};
+      UnitSpan sp{0, 0, 0};
       double msb = 0.0;
       const T *srcb = nullptr, *pub = nullptr, *pvb = nullptr;
       if (lane < kBatch && ub_unit < nunits) {
@@ -280,16 +279,19 @@ k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t ttr, int64_t tte, int merge, int64_
           vb = vv[ib];
           msb = ms[ib];
         }
-        sp = unit_span(tb, ttr, tte, merge, TILE, a.test_off, a.pitch);
-        srcb = (ib == redirect) ? elite_prev : S + ib * a.pitch;
-        pub = pool + ub * a.pitch;
-        pvb = pool + vb * a.pitch;
+        sp = unit_span(tb, a.lay);
+        srcb = ((ib == redirect) ? elite_prev : S + ib * a.lay.pitch) + sp.off;
+        pub = pool + ub * a.lay.pitch + sp.off;
+        pvb = pool + vb * a.lay.pitch + sp.off;
       }
       for (int q = 0; q < kBatch; ++q, ++k) {
         const int64_t unit = base + q;
-        const int t = __shfl_sync(0xffffffffu, (int)tb, q), i = __shfl_sync(0xffffffffu, (int)ib, q);
-        const int nA = __shfl_sync(0xffffffffu, sp.nA, q), nB = __shfl_sync(0xffffffffu, sp.nB, q);
-        const int64_t offA = __shfl_sync(0xffffffffu, sp.offA, q), offB = __shfl_sync(0xffffffffu, sp.offB, q);
+        // packed: (row, tile) in one 64-bit and (n, nA) (<= 8192 each) in one 32-bit shuffle
+        const uint64_t ti = __shfl_sync(0xffffffffu, ((uint64_t)tb << 32) | (uint32_t)ib, q);
+        const uint32_t nn = __shfl_sync(0xffffffffu, ((uint32_t)sp.n << 16) | (uint32_t)sp.nA, q);
+        const int t = (int)(ti >> 32), i = (int)(uint32_t)ti;
+        const int n = (int)(nn >> 16), nA = (int)(nn & 0xffffu);
+        const int64_t off = __shfl_sync(0xffffffffu, sp.off, q);
         const T* src = reinterpret_cast<const T*>(__shfl_sync(0xffffffffu, (unsigned long long)srcb, q));
         const T* pu = reinterpret_cast<const T*>(__shfl_sync(0xffffffffu, (unsigned long long)pub, q));
         const T* pv = reinterpret_cast<const T*>(__shfl_sync(0xffffffffu, (unsigned long long)pvb, q));
@@ -300,24 +302,17 @@ k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t ttr, int64_t tte, int merge, int64_
             slot_unit[s] = -1;
             mbar_arrive(full + s);
           } else {
-            const uint32_t bA = (uint32_t)nA * (uint32_t)sizeof(T), bB = (uint32_t)nB * (uint32_t)sizeof(T);
+            const uint32_t bytes = (uint32_t)n * (uint32_t)sizeof(T);
             T* d = data + (int64_t)s * 3 * TILE;
             slot_unit[s] = unit;
             slot_ms[s] = msd;
-            slot_it[s] = make_int4(i, t, nA, nB);
-            slot_off[s] = make_longlong2(offA, offB);
-            mbar_expect_tx(full + s, (kSseOnly ? 1 : 3) * (bA + bB));
-            bulk_g2s(d, src + offA, bA, full + s, stream);
+            slot_it[s] = make_int4(i, t, n, nA);
+            slot_off[s] = off;
+            mbar_expect_tx(full + s, (kSseOnly ? 1 : 3) * bytes);
+            bulk_g2s(d, src, bytes, full + s, stream);
             if (!kSseOnly) {
-              bulk_g2s(d + TILE, pu + offA, bA, full + s, keep);
-              bulk_g2s(d + 2 * TILE, pv + offA, bA, full + s, keep);
-            }
-            if (nB) {   // merged test tail, staged right after segment A
-              bulk_g2s(d + nA, src + offB, bB, full + s, stream);
-              if (!kSseOnly) {
-                bulk_g2s(d + TILE + nA, pu + offB, bB, full + s, keep);
-                bulk_g2s(d + 2 * TILE + nA, pv + offB, bB, full + s, keep);
-              }
+              bulk_g2s(d + TILE, pu, bytes, full + s, keep);
+              bulk_g2s(d + 2 * TILE, pv, bytes, full + s, keep);
             }
           }
         }
@@ -354,8 +349,8 @@ k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t ttr, int64_t tte, int merge, int64_
         }
         mbar_arrive(rempty + rs);
         const int64_t t = unit / m, i = unit - t * m;
-        a.part[(i * ntiles + t) * 2] = x;
-        a.part[(i * ntiles + t) * 2 + 1] = z;
+        a.part[(i * a.lay.ntiles + t) * 2] = x;
+        a.part[(i * a.lay.ntiles + t) * 2 + 1] = z;
         if (a.emax) {   // canonical-sum anchors, so the reduce reads the partials once
           if (x != 0.0) atomicMax(a.emax + 2 * i, canon_exp(x));
           if (z != 0.0) atomicMax(a.emax + 2 * i + 1, canon_exp(z));
@@ -386,17 +381,14 @@ k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t ttr, int64_t tte, int merge, int64_
     }
     const int4 it = slot_it[s];
     const int64_t t = it.y, i = it.x;
-    const int nA = it.z, n = it.z + it.w;               // segment B (merged test tail): [nA, n)
-    const longlong2 so = slot_off[s];
-    const int64_t offA = so.x, dB = so.y - nA;          // storage offset of element e: e + (e < nA ? offA : dB)
-    const bool trA = t < ttr;                            // segment A is train; segment B is always test
+    const int n = it.z, nA = it.w;                      // elements [0, nA) are train cases
+    const int64_t off = slot_off[s];
     if (t != cur_t) {   // target tile: registers, reloaded when the CTA changes tile
 #pragma unroll
       for (int q = 0; q < VPT; ++q) {
         const int e = (q * kNCT + ct) * EV;
-        const int64_t g = e + (e < nA ? offA : dB);
 #pragma unroll
-        for (int c = 0; c < EV; ++c) y[q][c] = e < n ? __ldg(a.y + g + c) : 0.0;
+        for (int c = 0; c < EV; ++c) y[q][c] = e < n ? __ldg(a.y + off + e + c) : 0.0;
       }
       cur_t = t;
     }
@@ -417,51 +409,37 @@ k_gsm_tma(GsmArgs a, int64_t ntiles, int64_t ttr, int64_t tte, int merge, int64_
     if (lane == 0) mbar_arrive(empty + s);   // stage free: the producer refills while we compute
     if (++s == kStages) { s = 0; ++j; }
 
+    T* orow = S + i * a.lay.pitch + off;
     double acc_tr = 0.0, acc_te = 0.0;
-    // the unit body, specialised for a plain tile (one segment: the hot
-    // path, no per-vector segment logic) and for the merged tail unit
-    auto body = [&](auto merged) {
-      constexpr bool kMerged = decltype(merged)::value;
-      T* orow = S + i * a.pitch + (kMerged ? 0 : offA);
-      T* erow = elite_cur + (kMerged ? 0 : offA);
 #pragma unroll
-      for (int q = 0; q < VPT; ++q) {
-        const int e = (q * kNCT + ct) * EV;
-        if (e >= n) continue;
-        const T* pe = reinterpret_cast<const T*>(&P[q]);
-        const T* ae = reinterpret_cast<const T*>(&A[q]);
-        const T* be = reinterpret_cast<const T*>(&B[q]);
-        Vec O;
-        T* oe = reinterpret_cast<T*>(&O);
-        double sacc = 0.0;
+    for (int q = 0; q < VPT; ++q) {
+      const int e = (q * kNCT + ct) * EV;
+      if (e >= n) continue;
+      const T* pe = reinterpret_cast<const T*>(&P[q]);
+      const T* ae = reinterpret_cast<const T*>(&A[q]);
+      const T* be = reinterpret_cast<const T*>(&B[q]);
+      Vec O;
+      T* oe = reinterpret_cast<T*>(&O);
+      double sacc = 0.0;
 #pragma unroll
-        for (int c = 0; c < EV; ++c) {
-          T o = kSseOnly ? pe[c] : mut(pe[c], ae[c], be[c], msv, a.sign);
-          if (kOp && !isfinite((double)o)) { o = (T)0; ++nonfinite; }
-          oe[c] = o;
-          const double dd = __dsub_rn((double)o, y[q][c]);
-          sacc = __fma_rn(dd, dd, sacc);   // one fused op: fewer fp64 issues (power-bound)
-        }
-        const bool inA = !kMerged || e < nA;
-        const int64_t g = kMerged ? e + (inA ? offA : dB) : e;
-        if (!kSseOnly) {
-          __stcs(reinterpret_cast<Vec*>(orow + g), O);
-          if (save) __stcs(reinterpret_cast<Vec*>(erow + g), P[q]);
-        }
-        if (inA && trA) acc_tr = __dadd_rn(acc_tr, sacc);
-        else acc_te = __dadd_rn(acc_te, sacc);
+      for (int c = 0; c < EV; ++c) {
+        T o = kSseOnly ? pe[c] : mut(pe[c], ae[c], be[c], msv, a.sign);
+        if (kOp && !isfinite((double)o)) { o = (T)0; ++nonfinite; }
+        oe[c] = o;
+        const double dd = __dsub_rn((double)o, y[q][c]);
+        sacc = __fma_rn(dd, dd, sacc);   // one fused op: fewer fp64 issues (power-bound)
       }
-    };
-    // fixed-order warp reduction; a plain tile is wholly train or test
-    if (n == nA) {
-      body(std::false_type{});
-      if (trA) acc_tr = warp_sum(acc_tr);
-      else acc_te = warp_sum(acc_te);
-    } else {
-      body(std::true_type{});
-      acc_tr = warp_sum(acc_tr);
-      acc_te = warp_sum(acc_te);
+      if (!kSseOnly) {
+        __stcs(reinterpret_cast<Vec*>(orow + e), O);
+        if (save) __stcs(reinterpret_cast<Vec*>(elite_cur + off + e), P[q]);
+      }
+      if (e < nA) acc_tr = __dadd_rn(acc_tr, sacc);
+      else acc_te = __dadd_rn(acc_te, sacc);
     }
+    // fixed-order warp reduction; a plain tile is wholly train or test
+    if (nA >= n) acc_tr = warp_sum(acc_tr);
+    else if (nA == 0) acc_te = warp_sum(acc_te);
+    else { acc_tr = warp_sum(acc_tr); acc_te = warp_sum(acc_te); }
     if (lane == 0) {
       if (k >= kRedStages) mbar_wait(rempty + rs, (rj & 1) ^ 1);
       red[(rs * kConsumerWarps + warp) * 2] = acc_tr;
@@ -483,24 +461,34 @@ int g_num_sms = 0;
 
 }  // namespace
 
-namespace {
-struct Tiling {
-  int64_t ttr, tte, ntiles;
-  int merge;
-};
-Tiling tiling(int64_t pitch, int64_t test_off, bool f64) {
-  const int64_t tile = kTileBytes / (f64 ? 8 : 4), nte = pitch - test_off;
-  Tiling t;
-  t.ttr = (test_off + tile - 1) / tile;
-  t.tte = (nte + tile - 1) / tile;
-  const int64_t tail_tr = test_off % tile, tail_te = nte % tile;
-  t.merge = (tail_tr > 0 && tail_te > 0 && tail_tr + tail_te <= tile) ? 1 : 0;
-  t.ntiles = t.ttr + t.tte - t.merge;
-  return t;
+RowLayout make_layout(int64_t ntr, int64_t nte, bool f64, bool allow_merge) {
+  auto pad32 = [](int64_t x) { return (x + 31) / 32 * 32; };
+  RowLayout L{};
+  L.tile = kTileBytes / (f64 ? 8 : 4);
+  L.ntr = ntr;
+  L.nte = nte;
+  L.ntr_pad = pad32(ntr);
+  const int64_t tail_tr = L.ntr_pad % L.tile, tail_te = nte % L.tile;
+  const bool merge = allow_merge && tail_tr > 0 && tail_te > 0 && tail_tr + pad32(tail_te) <= L.tile;
+  L.ttr = (L.ntr_pad + L.tile - 1) / L.tile;
+  if (merge) {   // [train | test tail | full test tiles]
+    L.tail_off = L.ntr_pad;
+    L.tail_pad = pad32(tail_te);
+    L.te_full = nte - tail_te;
+    L.test_off = L.tail_off + L.tail_pad;
+    L.pitch = L.test_off + L.te_full;
+    L.tte = L.te_full / L.tile;
+  } else {       // [train | test]
+    L.tail_off = -1;
+    L.tail_pad = 0;
+    L.te_full = nte;
+    L.test_off = L.ntr_pad;
+    L.pitch = L.test_off + pad32(nte);
+    L.tte = (pad32(nte) + L.tile - 1) / L.tile;
+  }
+  L.ntiles = L.ttr + L.tte;
+  return L;
 }
-}  // namespace
-
-int64_t gsm_tiles(int64_t pitch, int64_t test_off, bool f64) { return tiling(pitch, test_off, f64).ntiles; }
 
 int64_t gsm_tile_cases(bool f64) { return kTileBytes / (f64 ? 8 : 4); }
 
@@ -511,11 +499,9 @@ void launch_gsm(const GsmArgs& a, bool f64, bool operator_mode, cudaStream_t s) 
 void launch_sse_only(const GsmArgs& a, bool f64, cudaStream_t s) { launch_gsm_mode(a, f64, 2, s); }
 
 void launch_gsm_mode(const GsmArgs& a, bool f64, int mode, cudaStream_t s) {
-  if (a.m <= 0 || a.pitch <= 0) return;
-  GSGP_REQUIRE(a.pitch % 32 == 0, "storage pitch must be a multiple of 32");
-  GSGP_REQUIRE(a.test_off >= 0 && a.test_off <= a.pitch && a.test_off % 32 == 0, "bad test region offset");
-  const Tiling tl = tiling(a.pitch, a.test_off, f64);
-  const int64_t ntiles = tl.ntiles;
+  if (a.m <= 0 || a.lay.pitch <= 0) return;
+  GSGP_REQUIRE(a.lay.pitch % 32 == 0 && a.lay.tile == kTileBytes / (f64 ? 8 : 4), "bad storage layout");
+  const int64_t ntiles = a.lay.ntiles;
   if (g_num_sms == 0) {
     int dev = 0;
     GSGP_CUDA(cudaGetDevice(&dev));
@@ -534,7 +520,7 @@ void launch_gsm_mode(const GsmArgs& a, bool f64, int mode, cudaStream_t s) {
   if (forced > 0) batch = forced < 32 ? forced : 32;   // one unit per producer lane
   auto go = [&](auto kern) {
     GSGP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
-    kern<<<grid, kTmaThreads, kTmaSmem, s>>>(a, ntiles, tl.ttr, tl.tte, tl.merge, nunits, batch);
+    kern<<<grid, kTmaThreads, kTmaSmem, s>>>(a, nunits, batch);
   };
   if (f64) {
     if (mode == 1) go(k_gsm_tma<double, true>);

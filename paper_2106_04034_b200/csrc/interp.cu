@@ -316,7 +316,8 @@ __global__ void __launch_bounds__(NT) k_interpret(InterpArgs a, int64_t gpb,
     const int64_t q = q0 + c * NT + tid;
     train[c] = q < a.ntr;
     valid[c] = l0 + c * NT + tid < a.nq && (train[c] || q >= a.te_q);   // [ntr, te_q): gap
-    col[c] = train[c] ? q : a.test_off + (q - a.te_q);
+    const int64_t j = q - a.te_q;                       // test case index
+    col[c] = train[c] ? q : (j < a.te_full ? a.test_off + j : a.tail_off + (j - a.te_full));
     ytr[c] = (MODE == INTERP_POP && valid[c]) ? a.y[col[c]] : 0.0;
   }
   const double* xg = a.XT + l0 + tid;          // global feature rows (!kXSmem)

@@ -92,9 +92,11 @@ struct InterpArgs {
   double* out64;            // INTERP_F64: [count][ntr+nte]
   void* out;                // INTERP_POP/POOL: [count][pitch] float or double
   int32_t out_is_f64;
-  int64_t pitch;            // storage pitch (elements); test region starts at test_off
-  int64_t test_off;
-  const double* y;          // targets in storage layout (pitch, test at test_off) (INTERP_POP)
+  int64_t pitch;            // storage pitch (elements)
+  int64_t test_off;         // test case j stored at test_off + j (j < te_full) ...
+  int64_t te_full;
+  int64_t tail_off;         // ... else at tail_off + (j - te_full) (RowLayout)
+  const double* y;          // targets in storage layout (INTERP_POP)
   double* part;             // [count][ntiles][2] SSE partials (INTERP_POP)
   int32_t* wide;            // [count] bit0 train overflowed fp32, bit1 test (INTERP_POP)
   unsigned long long* nonfinite;   // element count replaced by 0.0
@@ -104,6 +106,30 @@ struct InterpArgs {
 int64_t interp_tiles(const InterpArgs& a, int* tile_out);
 void launch_interpret(const InterpArgs& a, int mode, cudaStream_t s);
 
+// ------------------------------------------------------------ storage rows
+// One shard's semantics row (pitch elements, fp32 or fp64): the train cases
+// [0, ntr) (region padded to ntr_pad), then the test cases.  Generation
+// units are `tile`-case tiles anchored on the train region and on the test
+// region separately.  When the partial train tail and the partial test tail
+// fit in one tile together, the test tail is stored right after the train
+// region — [train | test tail | full test tiles] — so the two tails form ONE
+// contiguous unit (gsm.cu unit_span); otherwise [train | test].  Test case j
+// lives at test_off + j for j < te_full, else at tail_off + (j - te_full).
+struct RowLayout {
+  int64_t ntr, nte;
+  int64_t ntr_pad;          // train region [0, ntr_pad), zero padded
+  int64_t tail_off;         // relocated test tail (-1: none), tail_pad elements
+  int64_t tail_pad;
+  int64_t te_full;          // test cases stored from test_off on
+  int64_t test_off;
+  int64_t pitch;
+  int64_t tile, ttr, tte, ntiles;   // units per row: ttr train units (the last may carry the test tail) + tte
+};
+RowLayout make_layout(int64_t ntr, int64_t nte, bool f64, bool allow_merge = true);
+__host__ __device__ inline int64_t test_col(const RowLayout& L, int64_t j) {
+  return j < L.te_full ? L.test_off + j : L.tail_off + (j - L.te_full);
+}
+
 // ------------------------------------------------------------ generation
 struct GsmArgs {
   const void* pool;         // [r][pitch] squashed trees (float or double)
@@ -111,14 +137,14 @@ struct GsmArgs {
   const void* elite_prev;   // [pitch] saved parent elite row (redirect target)
   void* elite_cur;          // [pitch] parent row b_p is saved here
   const double* y;          // [pitch] targets in storage layout (0 in padding)
-  int64_t pitch, test_off;
+  RowLayout lay;            // storage row layout (units, pitch)
   int64_t m;
   const int64_t* u;         // plan of this generation (or base when gen_ptr != nullptr)
   const int64_t* v;
   const double* ms;
   const int64_t* ctl;       // device control block (see engine.cu), may be nullptr
   int32_t sign;             // 0 minus, 1 plus
-  double* part;             // [m][gsm_tiles][2]
+  double* part;             // [m][lay.ntiles][2]
   int32_t* emax;            // optional [m][2]: atomicMax of the partials' canon_exp (fused tail);
                             // must hold kExpZero before the launch (the reduce resets it)
   unsigned long long* nonfinite;   // operator mode only
@@ -132,10 +158,6 @@ struct GsmArgs {
   int32_t write_plan;
   PlanParams plan;
 };
-// units per row (the part[] row stride): train tiles over [0, test_off),
-// then test tiles over [test_off, pitch), the two partial tails merged into
-// one unit when they fit (gsm.cu unit_span); cases per tile
-int64_t gsm_tiles(int64_t pitch, int64_t test_off, bool f64);
 int64_t gsm_tile_cases(bool f64);
 void launch_gsm(const GsmArgs& a, bool f64, bool operator_mode, cudaStream_t s);
 // SSE of the stored semantics S against y in the generation kernel's exact
