@@ -66,19 +66,54 @@ def _round_scaled(S: int, scale: int) -> float:
         return math.inf
 
 
-def canonical_sum(values) -> float:
-    """Order-free sum of one row of non-negative fp64 partials."""
+LIMBS = 4
+EXP_ZERO = -0x7F7F7F80        # common.cuh kExpZero / kExpInf / kExpNaN
+EXP_INF = 0x7FFFFFF0
+EXP_NAN = 0x7FFFFFFF
+
+
+def anchor(values) -> int:
+    """The row's anchor key: max canon_exp over the partials, with the
+    special keys for NaN / +inf / all-zero (common.cuh canon_exp)."""
     v = np.asarray(values, dtype=np.float64).ravel()
     if np.isnan(v).any():
-        return math.nan
+        return EXP_NAN
     if np.isinf(v).any():
+        return EXP_INF
+    nz = v[v > 0.0]
+    return max(canon_exp(float(x)) for x in nz) if nz.size else EXP_ZERO
+
+
+def digits(values, A: int) -> list[int]:
+    """Digit-limb sums of floor(v * 2^(116 - A)) (common.cuh canon_add):
+    limb d = sum of the 32-bit digits d of every X.  Limb sums are plain
+    integer additions, so they can be split over ranks in any grouping."""
+    out = [0] * LIMBS
+    if A >= EXP_INF or A == EXP_ZERO:
+        return out
+    for x in np.asarray(values, dtype=np.float64).ravel():
+        if x > 0.0:
+            X = _fixed(float(x), A)
+            for d in range(LIMBS):
+                out[d] += (X >> (32 * d)) & 0xFFFFFFFF
+    return out
+
+
+def finish(limbs, A: int) -> float:
+    """Round sum(limbs[d] * 2^(32 d)) * 2^(A - 116) once (common.cuh canon_finish)."""
+    if A == EXP_NAN:
+        return math.nan
+    if A == EXP_INF:
         return math.inf
-    nz = [float(x) for x in v if x > 0.0]
-    if not nz:
+    if A < -1100:
         return 0.0
-    A = max(canon_exp(x) for x in nz)
-    S = sum(_fixed(x, A) for x in nz)
-    return _round_scaled(S, A - ANCHOR)
+    return _round_scaled(sum(int(l) << (32 * d) for d, l in enumerate(limbs)), A - ANCHOR)
+
+
+def canonical_sum(values) -> float:
+    """Order-free sum of one row of non-negative fp64 partials."""
+    A = anchor(values)
+    return finish(digits(values, A), A)
 
 
 def canonical_rows(M) -> np.ndarray:
