@@ -714,7 +714,7 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
       a.sign = cfg->gsm_sign;
       a.part = p->part.as<double>();
       a.ticket = p->ticket.as<unsigned long long>();
-      a.emax = fused_tail ? gemax.as<int32_t>() : nullptr;
+      a.emax = (fused_tail && p->ntiles > 1) ? gemax.as<int32_t>() : nullptr;   // single unit: SSE = partial
       a.plan_inline = 1;
       a.write_plan = plan_written ? 0 : 1;   // the first non-empty shard records the plan
       plan_written = true;

@@ -201,7 +201,8 @@ struct SurviveArgs {
 void launch_survive(const SurviveArgs& a, cudaStream_t s);
 // per-row canonical SSE into sse (== a.sse_off) fused with survival (single
 // shard, single rank); emax = the anchors the GSM launch accumulated (reset
-// to kExpZero here); `done` is a zeroed counter, re-zeroed on exit
+// to kExpZero here; unused when ntiles == 1: the SSE is the partial itself);
+// `done` is a zeroed counter, re-zeroed on exit
 void launch_reduce_survive(const double* part, int64_t ntiles, int32_t* emax, double* sse,
                            const SurviveArgs& a, unsigned int* done, cudaStream_t s);
 // initial elite: fitness from SSE, argmin, trace[0] (evolution.py:132-143)

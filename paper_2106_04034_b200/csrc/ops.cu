@@ -412,6 +412,25 @@ __global__ void __launch_bounds__(256) k_reduce_survive(const double* __restrict
   if (threadIdx.x == 0) *done = 0;
 }
 
+// one unit per row (small case counts, e.g. C1): the canonical sum of a
+// single partial is that partial, bit for bit (its fixed-point image is
+// exact), so the SSE is copied and no anchors are used
+__global__ void __launch_bounds__(256) k_reduce_survive_single(const double* __restrict__ part,
+                                                               double* __restrict__ sse, SurviveArgs a,
+                                                               unsigned int* done) {
+  __shared__ int last;
+  const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;   // (row, train|test)
+  if (i < 2 * a.m) sse[i] = part[i];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  survive_block(a);
+  if (threadIdx.x == 0) *done = 0;
+}
+
 __global__ void __launch_bounds__(256) k_reduce_survive_wide(const double* __restrict__ part, int64_t ntiles,
                                                              int32_t* emax, double* __restrict__ sse,
                                                              SurviveArgs a, unsigned int* done) {
@@ -567,7 +586,9 @@ void launch_row_rmse(const double* S, const double* y, int64_t m, int64_t n, dou
 
 void launch_reduce_survive(const double* part, int64_t ntiles, int32_t* emax, double* sse,
                            const SurviveArgs& a, unsigned int* done, cudaStream_t s) {
-  if (ntiles > 256)    // long rows (C3 ~3000 tiles): a block per row; else a warp (8 loads per lane)
+  if (ntiles == 1)     // emax is not used (the generation launch leaves it untouched)
+    k_reduce_survive_single<<<(unsigned)((2 * a.m + 255) / 256), 256, 0, s>>>(part, sse, a, done);
+  else if (ntiles > 256)   // long rows (C3 ~3000 tiles): a block per row; else a warp (8 loads per lane)
     k_reduce_survive_wide<<<(unsigned)a.m, 256, 0, s>>>(part, ntiles, emax, sse, a, done);
   else
     k_reduce_survive<<<(unsigned)((a.m + 7) / 8), 256, 0, s>>>(part, ntiles, emax, sse, a, done);
