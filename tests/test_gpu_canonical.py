@@ -133,3 +133,31 @@ def test_ranks_bit_identical_to_single_process(world, vshards, wide):
     assert sum(1 for lo, hi in spans if hi > lo) >= 2        # the cases really are split
     for rank, fp, _ in got:
         assert fp == base, rank
+
+
+@pytest.mark.parametrize("ntr,nte,storage", [
+    (4096, 4096, "fp32"),            # no tails
+    (4096 * 3 + 1, 4095, "fp32"),    # tails 1 + 4095 (do not fit one tile together)
+    (12288 * 2 + 4064, 32, "fp32"),  # tails 4064 + 32 fill one tile exactly
+    (24576 + 7, 12288 + 9, "fp32"),  # tails on both shard-grid boundaries
+    (2048 * 5 + 100, 2048 + 1900, "fp64"),   # fp64 tiles (2048 cases)
+    (12288 * 3, 12288, "fp64"),
+])
+def test_tile_and_shard_boundaries(ntr, nte, storage):
+    """Row layouts around the tile and shard-grid boundaries (tails absent,
+    merged, too large to merge): every virtual-shard count reproduces the
+    one-shard run bit for bit, and the elite trace matches the engine
+    restatement (oracle/engine32.py) run on the host."""
+    from oracle import engine32, restate as R
+    rng = np.random.default_rng(ntr + nte)
+    Xtr, Xte = rng.uniform(-1, 1, (ntr, 3)), rng.uniform(-1, 1, (nte, 3))
+    f = lambda X: X[:, 0] * X[:, 1] - X[:, 2]
+    kw = dict(population_size=12, random_trees=6, program_size=31, generations=6, seed=ntr % 97 + 1)
+    cfg = G.RunConfig(**kw)
+    tr, te = G.Dataset(Xtr, f(Xtr)), G.Dataset(Xte, f(Xte))
+    base = _fingerprint(G.run_evolution(cfg, tr, te, storage=storage))
+    for vs in (2, 3, 4):
+        assert _fingerprint(G.run_evolution(cfg, tr, te, storage=storage, virtual_shards=vs)) == base, vs
+    if storage == "fp32":
+        o = engine32.run32(R.Cfg(**kw), Xtr, f(Xtr), Xte, f(Xte))
+        assert base[0] == [e[:3] for e in o["elite"]]
