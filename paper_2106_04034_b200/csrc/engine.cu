@@ -382,7 +382,7 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   codes.alloc(ng * k * 4);
   consts.alloc(ng * k * 8);
   ins.alloc(ng * (k + 1) * sizeof(Ins));
-  exe.alloc(ng * (k + 1) * sizeof(Ins));
+  exe.alloc(2 * ng * (k + 1) * sizeof(Ins));   // two linked copies (grouped interpreter blocks)
   plen.alloc(ng * 4);
   pnconst.alloc(ng * 4);
   ctab.alloc(ng * k * 8);
@@ -464,6 +464,7 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
     InterpArgs ia{};
     ia.code = ins.as<Ins>();
     ia.exe = exe.as<Ins>();
+    ia.exe_gstride = ng * (k + 1);
     ia.len = plen.as<int32_t>();
     ia.nconst = pnconst.as<int32_t>();
     ia.ctab = ctab.as<double>();

@@ -203,28 +203,38 @@ struct InterpCfg {
   bool xsmem;   // features of the tile in shared memory (else read from HBM/L2)
   bool lean;    // program and constants stay in HBM: only the spill rows use
                 // shared memory, so any program size fits (huge k fallback)
+  int groups = 1;   // genome groups per block sharing one staged feature tile
+                    // (each group: nt threads, its own spill/constant rows + program)
 };
 constexpr InterpCfg kCfgs[] = {{128, 4, true, false}, {64, 8, true, false}, {128, 4, false, false},
-                               {128, 2, true, false}, {128, 1, false, true}, {128, 3, true, false}};
+                               {128, 2, true, false}, {128, 1, false, true}, {128, 3, true, false},
+                               {128, 3, true, false, 2}};
 constexpr int kNumCfgs = sizeof(kCfgs) / sizeof(kCfgs[0]);
 constexpr size_t kSmemCap = 200 * 1024;
 
 // rows of the case tile + the staged program (16 B per instruction)
+// rows of one genome group: spill slots + constant rows
+size_t cfg_group_rows(const InterpCfg& c, const InterpArgs& a) {
+  const size_t crows = c.lean ? 0 : ((size_t)(a.maxconst > 0 ? a.maxconst : 1) + c.nt - 1) / c.nt;
+  return (size_t)a.maxdepth + crows;
+}
 size_t cfg_rows_bytes(const InterpCfg& c, const InterpArgs& a) {
   const size_t rowb = (size_t)c.nt * c.cpt * 8;
-  const size_t crows = c.lean ? 0 : ((size_t)(a.maxconst > 0 ? a.maxconst : 1) + c.nt - 1) / c.nt;
-  return ((c.xsmem ? (size_t)a.l : 0) + (size_t)a.maxdepth + crows) * rowb;
+  return ((c.xsmem ? (size_t)a.l : 0) + c.groups * cfg_group_rows(c, a)) * rowb;
 }
+// + 1 instruction per program: the loop prefetches one past the end
+size_t cfg_prog_bytes(const InterpArgs& a) { return (size_t)((a.maxlen > 0 ? a.maxlen : 1) + 1) * sizeof(Ins); }
 size_t cfg_smem(const InterpCfg& c, const InterpArgs& a) {
   if (c.lean) return cfg_rows_bytes(c, a) + 16;
-  // + 1 instruction: the loop prefetches one past the end of the program
-  return cfg_rows_bytes(c, a) + (size_t)((a.maxlen > 0 ? a.maxlen : 1) + 1) * sizeof(Ins);
+  return cfg_rows_bytes(c, a) + c.groups * cfg_prog_bytes(a);
 }
 
 int choose_cfg(const InterpArgs& a) {
   const char* env = getenv("GSGP_INTERP_CFG");   // experiments / tests (read per launch)
   const int forced = env ? atoi(env) : -1;
-  if (forced >= 0 && forced < kNumCfgs && cfg_smem(kCfgs[forced], a) <= kSmemCap) return forced;
+  if (forced >= 0 && forced < kNumCfgs && cfg_smem(kCfgs[forced], a) <= kSmemCap &&
+      (kCfgs[forced].groups == 1 || a.exe_gstride > 0))
+    return forced;
   // features in shared memory while the tile keeps >= 3 blocks per SM; the
   // 384-case tile (128 x 3) fits 5 blocks (20 warps) where 128 x 4 fits 4:
   // measured 1-4 % faster (profiles/r01/README.md)
@@ -239,20 +249,24 @@ int choose_cfg(const InterpArgs& a) {
 // abstract operand -> byte offset in the block's shared-memory row layout:
 // rows [0, l) features (xsmem), then maxdepth spill slots, then constant rows
 // (constant j: row j / nt, lane j % nt, replicated for the CPT cases)
+// (grouped blocks: group gi's rows start grows * gi rows later; its linked
+// copy is written at exe + gi * gstride)
 __global__ void k_link(const Ins* __restrict__ code, Ins* __restrict__ exe, const int32_t* __restrict__ len,
                        int64_t count, int64_t k1, int32_t nt, uint32_t rowb, uint32_t frows,
-                       uint32_t maxdepth, bool lean) {
+                       uint32_t maxdepth, bool lean, int groups, uint32_t grows, int64_t gstride) {
   const int64_t g = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;   // one warp per genome
   if (g >= count) return;
   const int32_t n = len[g];
+  for (int gi = 0; gi < groups; ++gi) {
+  const uint32_t gb = frows + (uint32_t)gi * grows;   // first row of this group
   // byte offset of an operand; vec = 1 for a per-case row, 0 for a constant
   auto off = [&](uint32_t cls, uint32_t idx, uint32_t& vec) -> uint32_t {
     vec = 1;
     if (cls == X_FEAT) return frows ? idx * rowb : (kFeatGlobal | idx);
-    if (cls == X_STACK) return (frows + idx) * rowb;
+    if (cls == X_STACK) return (gb + idx) * rowb;
     vec = 0;
     if (lean) return kConstGlobal | idx;
-    return (frows + maxdepth + idx / (uint32_t)nt) * rowb + (idx % (uint32_t)nt) * 8u;
+    return (gb + maxdepth + idx / (uint32_t)nt) * rowb + (idx % (uint32_t)nt) * 8u;
   };
   for (int32_t i = threadIdx.x % 32; i < n; i += 32) {
     const Ins in = code[g * k1 + i];
@@ -266,7 +280,8 @@ __global__ void k_link(const Ins* __restrict__ code, Ins* __restrict__ exe, cons
     // d: x lane mask in the low bits (tid*8 < 1024), y-is-vector bit 16,
     // push slot from bit 20 — so the interpreter uses a as the jump index as is
     o.d = (xvec ? 0x3ffu : 0u) | (yvec << 16) | (push << 20);
-    exe[g * k1 + i] = o;
+    exe[gi * gstride + g * k1 + i] = o;
+  }
   }
 }
 
@@ -286,14 +301,30 @@ __device__ __forceinline__ uint4 lds_u128(uint32_t p) {
 }
 
 
-template <int NT, int CPT, int MODE, typename TOut, bool kXSmem, bool kLean>
-__global__ void __launch_bounds__(NT) k_interpret(InterpArgs a, int64_t gpb,
-                                                  uint32_t stack_off, uint32_t crow_off,
-                                                  uint32_t prog_off) {
+// block barrier of one genome group (GROUPS > 1: named barrier 1 + group)
+template <int GROUPS, int NT>
+__device__ __forceinline__ void group_sync(int grp) {
+  if constexpr (GROUPS == 1) __syncthreads();
+  else asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(NT) : "memory");
+}
+
+// GROUPS > 1: the block runs GROUPS genome groups of NT threads on the same
+// case tile; the staged features are shared, each group has its own spill
+// and constant rows (grp_bytes apart) and program slot (prog_bytes apart),
+// linked for it by k_link (copy `grp` of the linked programs)
+template <int NT, int CPT, int MODE, typename TOut, bool kXSmem, bool kLean, int GROUPS>
+__global__ void __launch_bounds__(NT * GROUPS) k_interpret(InterpArgs a, int64_t gpb,
+                                                           uint32_t stack_off, uint32_t crow_off,
+                                                           uint32_t prog_off, uint32_t grp_bytes,
+                                                           uint32_t prog_bytes) {
   constexpr int TILE = NT * CPT;
   constexpr uint32_t CSTRIDE = NT * 8;          // bytes between a thread's cases
   extern __shared__ __align__(16) unsigned char smem[];
-  const int tid = threadIdx.x;
+  const int tid = GROUPS == 1 ? (int)threadIdx.x : (int)threadIdx.x % NT;
+  const int grp = GROUPS == 1 ? 0 : (int)threadIdx.x / NT;
+  stack_off += grp * grp_bytes;
+  crow_off += grp * grp_bytes;
+  prog_off += grp * prog_bytes;
   const uint32_t tid8 = (uint32_t)tid * 8u;
   const int64_t tile = blockIdx.x;             // tile of this launch's case range
   const int64_t l0 = tile * TILE;               // first case of the tile, launch-local
@@ -303,10 +334,11 @@ __global__ void __launch_bounds__(NT) k_interpret(InterpArgs a, int64_t gpb,
 
   if (kXSmem) {
     double* xs = reinterpret_cast<double*>(smem);
-    for (int64_t e = tid; e < (int64_t)a.l * TILE; e += NT) {
+    for (int64_t e = threadIdx.x; e < (int64_t)a.l * TILE; e += NT * GROUPS) {
       const int64_t f = e / TILE, c = e - f * TILE;
       xs[e] = l0 + c < a.nq ? a.XT[f * a.xt_pitch + l0 + c] : 0.0;
     }
+    if (GROUPS > 1) __syncthreads();            // the groups only sync among themselves below
   }
   double ytr[CPT];
   int64_t col[CPT];
@@ -353,15 +385,15 @@ __global__ void __launch_bounds__(NT) k_interpret(InterpArgs a, int64_t gpb,
 
   const int64_t g0 = blockIdx.y * gpb;
   const int64_t g1 = min(a.count, g0 + gpb);
-  for (int64_t g = g0; g < g1; ++g) {
+  for (int64_t g = g0 + grp; g < g1; g += GROUPS) {
     // ---- stage genome g: program + constant table (replicated for the CPT
     // cases of a thread) into shared memory
     const int len = a.len[g];
     cg = a.ctab + g * cstride;
-    __syncthreads();                            // previous genome done with both (and red[])
+    group_sync<GROUPS, NT>(grp);                // previous genome done with both (and red[])
     if (!kLean) {
     {
-      const uint4* src = reinterpret_cast<const uint4*>(a.exe + g * a.k1);
+      const uint4* src = reinterpret_cast<const uint4*>(a.exe + grp * a.exe_gstride + g * a.k1);
       uint4* dst = reinterpret_cast<uint4*>(smem + prog_off);
       for (int i = tid; i < len; i += NT) dst[i] = __ldg(src + i);
       const int nc = a.nconst[g];
@@ -372,7 +404,7 @@ __global__ void __launch_bounds__(NT) k_interpret(InterpArgs a, int64_t gpb,
                                    (uint32_t)(j % NT) * 8u + (uint32_t)c * CSTRIDE) = ct[j];
       }
     }
-    __syncthreads();
+    group_sync<GROUPS, NT>(grp);
     }
 
     double acc[CPT];
@@ -427,15 +459,16 @@ __global__ void __launch_bounds__(NT) k_interpret(InterpArgs a, int64_t gpb,
       sse_tr = warp_sum(sse_tr);
       sse_te = warp_sum(sse_te);
       int wb = __reduce_or_sync(0xffffffffu, wide);
+      double* gred = red + grp * (NT / 32) * 2;
       if ((tid & 31) == 0) {
-        red[(tid >> 5) * 2] = sse_tr;
-        red[(tid >> 5) * 2 + 1] = sse_te;
+        gred[(tid >> 5) * 2] = sse_tr;
+        gred[(tid >> 5) * 2 + 1] = sse_te;
         if (wb) atomicOr(a.wide + g, wb);
       }
-      __syncthreads();
+      group_sync<GROUPS, NT>(grp);
       if (tid < 2) {
         double t = 0.0;
-        for (int w = 0; w < NT / 32; ++w) t = __dadd_rn(t, red[w * 2 + tid]);
+        for (int w = 0; w < NT / 32; ++w) t = __dadd_rn(t, gred[w * 2 + tid]);
         a.part[(g * a.part_ntiles + a.q_base / TILE + tile) * 2 + tid] = t;
       }
     }
@@ -445,10 +478,12 @@ __global__ void __launch_bounds__(NT) k_interpret(InterpArgs a, int64_t gpb,
   if ((tid & 31) == 0 && nonfinite) atomicAdd(a.nonfinite, nonfinite);
 }
 
-template <int NT, int CPT, int MODE, typename TOut, bool kXSmem, bool kLean = false>
+template <int NT, int CPT, int MODE, typename TOut, bool kXSmem, bool kLean = false, int GROUPS = 1>
 void launch_cfg(const InterpArgs& a, cudaStream_t s) {
   constexpr int TILE = NT * CPT;
-  constexpr InterpCfg c{NT, CPT, kXSmem, kLean};
+  constexpr InterpCfg c{NT, CPT, kXSmem, kLean, GROUPS};
+  static_assert(GROUPS == 1 || (kXSmem && !kLean), "grouped blocks share a staged feature tile");
+  GSGP_REQUIRE(GROUPS == 1 || a.exe_gstride > 0, "grouped interpreter blocks need two linked copies");
   const int64_t ntiles = (a.nq + TILE - 1) / TILE;
   GSGP_REQUIRE(a.te_q >= a.ntr && (a.nte == 0 || a.te_q % TILE == 0 || a.te_q == a.ntr),
                "test cases must start on an interpreter tile");
@@ -458,8 +493,10 @@ void launch_cfg(const InterpArgs& a, cudaStream_t s) {
   const size_t smem = cfg_smem(c, a);
   GSGP_REQUIRE(smem <= kSmemCap, "interpreter tile does not fit in shared memory");
   // link the programs for this row layout
+  const uint32_t grows = (uint32_t)cfg_group_rows(c, a);
   k_link<<<(unsigned)((a.count + 3) / 4), 128, 0, s>>>(a.code, a.exe, a.len, a.count, a.k1, NT, rowb,
-                                                      frows, (uint32_t)a.maxdepth, kLean);
+                                                      frows, (uint32_t)a.maxdepth, kLean, GROUPS, grows,
+                                                      a.exe_gstride);
   GSGP_CUDA(cudaGetLastError());
   // genomes per block: enough blocks to fill 148 SMs several times over
   const int64_t want = 148 * 8;
@@ -469,21 +506,44 @@ void launch_cfg(const InterpArgs& a, cudaStream_t s) {
   const int64_t gy = (a.count + gpb - 1) / gpb;
   GSGP_REQUIRE(gy <= 65535, "too many genome groups");
   dim3 grid((unsigned)ntiles, (unsigned)gy);
-  auto k = k_interpret<NT, CPT, MODE, TOut, kXSmem, kLean>;
+  auto k = k_interpret<NT, CPT, MODE, TOut, kXSmem, kLean, GROUPS>;
   GSGP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k<<<grid, NT, smem, s>>>(a, gpb, frows * rowb, (frows + (uint32_t)a.maxdepth) * rowb,
-                           (uint32_t)cfg_rows_bytes(c, a));
+  k<<<grid, NT * GROUPS, smem, s>>>(a, gpb, frows * rowb, (frows + (uint32_t)a.maxdepth) * rowb,
+                                    (uint32_t)cfg_rows_bytes(c, a), grows * rowb,
+                                    (uint32_t)cfg_prog_bytes(a));
   GSGP_CUDA(cudaGetLastError());
+}
+
+// 128x3 tiles: two genome groups per block share the staged feature tile,
+// so when shared memory (not registers) limits the resident blocks the
+// grouped launch holds more warps per SM (C3: 24 vs 20) — chosen by the
+// occupancy calculator unless GSGP_INTERP_CFG forces a configuration
+template <int MODE, typename TOut>
+int grouped_or_single(const InterpArgs& a) {
+  if (a.exe_gstride <= 0 || getenv("GSGP_INTERP_CFG")) return 5;
+  const size_t s1 = cfg_smem(kCfgs[5], a), s2 = cfg_smem(kCfgs[6], a);
+  if (s2 > kSmemCap) return 5;
+  auto k1 = k_interpret<128, 3, MODE, TOut, true, false, 1>;
+  auto k2 = k_interpret<128, 3, MODE, TOut, true, false, 2>;
+  int b1 = 0, b2 = 0;
+  GSGP_CUDA(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1));
+  GSGP_CUDA(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2));
+  GSGP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k1, 128, s1));
+  GSGP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k2, 256, s2));
+  return b2 * 8 > b1 * 4 ? 6 : 5;
 }
 
 template <int MODE, typename TOut>
 void launch_mode(const InterpArgs& a, cudaStream_t s) {
-  switch (choose_cfg(a)) {
+  int cfg = choose_cfg(a);
+  if (cfg == 5) cfg = grouped_or_single<MODE, TOut>(a);
+  switch (cfg) {
     case 0: launch_cfg<128, 4, MODE, TOut, true>(a, s); break;
     case 1: launch_cfg<64, 8, MODE, TOut, true>(a, s); break;
     case 2: launch_cfg<128, 4, MODE, TOut, false>(a, s); break;
     case 3: launch_cfg<128, 2, MODE, TOut, true>(a, s); break;
     case 5: launch_cfg<128, 3, MODE, TOut, true>(a, s); break;
+    case 6: launch_cfg<128, 3, MODE, TOut, true, false, 2>(a, s); break;
     default: launch_cfg<128, 1, MODE, TOut, false, true>(a, s); break;
   }
 }

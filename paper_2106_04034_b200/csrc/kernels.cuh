@@ -73,6 +73,8 @@ enum InterpMode : int { INTERP_F64 = 0, INTERP_POP = 1, INTERP_POOL = 2 };
 struct InterpArgs {
   const Ins* code;          // abstract program (count genomes, stride k1)
   Ins* exe;                 // linked copy, rewritten by every launch_interpret
+  int64_t exe_gstride;      // elements between the per-group linked copies (0: one copy only;
+                            // grouped configurations need a second copy at exe + exe_gstride)
   const int32_t* len;
   const int32_t* nconst;
   const double* ctab;       // [count][k1 - 1]

@@ -394,7 +394,7 @@ def test_interpreter_division_fast_path_near_halfway_quotients():
     ref, _ = R.semantics(tags, codes, consts, X, 1e-6)
     pop = Population(tags, codes, consts)
     import os
-    for cfg in ("0", "1", "2", "3", "4", "5"):
+    for cfg in ("0", "1", "2", "3", "4", "5", "6"):
         os.environ["GSGP_INTERP_CFG"] = cfg
         try:
             S = G.compute_semantics(pop, X, RunConfig(program_size=k))

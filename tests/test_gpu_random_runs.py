@@ -54,8 +54,9 @@ def test_random_run_matches_engine_restatement(seed, monkeypatch):
     if seed % 4 == 1:
         monkeypatch.setenv("GSGP_UPLOAD_CHUNK", "3072")
     # every interpreter launch configuration takes part (0 128x4, 2 HBM
-    # features, 3 128x2, 4 lean, 5 128x3 default)
-    monkeypatch.setenv("GSGP_INTERP_CFG", "05234"[seed % 5])
+    # features, 3 128x2, 4 lean, 5 128x3, 6 128x3 with two genome groups per
+    # block — the default when shared memory limits the resident blocks)
+    monkeypatch.setenv("GSGP_INTERP_CFG", "052346"[seed % 6])
     res = G.run_evolution(G.RunConfig(**kw), G.Dataset(Xtr, ytr), G.Dataset(Xte, yte),
                           virtual_shards=1 + seed % 3)
     o = engine32.run32(R.Cfg(**kw), Xtr, ytr, Xte, yte)
