@@ -301,6 +301,9 @@ __device__ __forceinline__ uint4 lds_u128(uint32_t p) {
 }
 
 
+#ifndef GSGP_INTERP_MINB2   // min resident blocks of the grouped launch (register cap)
+#define GSGP_INTERP_MINB2 4
+#endif
 // block barrier of one genome group (GROUPS > 1: named barrier 1 + group)
 template <int GROUPS, int NT>
 __device__ __forceinline__ void group_sync(int grp) {
@@ -313,7 +316,7 @@ __device__ __forceinline__ void group_sync(int grp) {
 // and constant rows (grp_bytes apart) and program slot (prog_bytes apart),
 // linked for it by k_link (copy `grp` of the linked programs)
 template <int NT, int CPT, int MODE, typename TOut, bool kXSmem, bool kLean, int GROUPS>
-__global__ void __launch_bounds__(NT * GROUPS) k_interpret(InterpArgs a, int64_t gpb,
+__global__ void __launch_bounds__(NT * GROUPS, GROUPS == 2 ? GSGP_INTERP_MINB2 : 1) k_interpret(InterpArgs a, int64_t gpb,
                                                            uint32_t stack_off, uint32_t crow_off,
                                                            uint32_t prog_off, uint32_t grp_bytes,
                                                            uint32_t prog_bytes) {
@@ -530,6 +533,16 @@ int grouped_or_single(const InterpArgs& a) {
   GSGP_CUDA(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2));
   GSGP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k1, 128, s1));
   GSGP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k2, 256, s2));
+  if (getenv("GSGP_INTERP_TRACE")) {
+    cudaFuncAttributes f1{}, f2{};
+    cudaFuncGetAttributes(&f1, k1);
+    cudaFuncGetAttributes(&f2, k2);
+    int z2 = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&z2, k2, 256, 0);
+    fprintf(stderr, "interp cfg: single %d blocks (%zu B, %d regs, %zu static), grouped %d blocks (%zu B, %d regs,"
+            " %zu static, %d blocks without dynamic smem, max threads %d)\n", b1, s1, f1.numRegs,
+            f1.sharedSizeBytes, b2, s2, f2.numRegs, f2.sharedSizeBytes, z2, f2.maxThreadsPerBlock);
+  }
   return b2 * 8 > b1 * 4 ? 6 : 5;
 }
 
