@@ -194,7 +194,7 @@ int gsgp_compute_semantics(const uint8_t* tags, const int32_t* codes, const doub
     h2d(dt.p, tags, count * k);
     h2d(dc.p, codes, count * k * 4);
     h2d(dv.p, consts, count * k * 8);
-    Buf ins(count * (k + 1) * sizeof(Ins)), exe(2 * count * (k + 1) * sizeof(Ins)), len(count * 4),
+    Buf ins(count * (k + 1) * sizeof(Ins)), exe(kMaxInterpGroups * count * (k + 1) * sizeof(Ins)), len(count * 4),
         nconst(count * 4), ctab(count * k * 8), mx(3 * 4), scr(count * 4 * k * 4), fl(count * k),
         cv(count * k * 8);
     Program prog{ins.as<Ins>(), exe.as<Ins>(), len.as<int32_t>(), nconst.as<int32_t>(),

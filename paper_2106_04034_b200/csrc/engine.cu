@@ -382,7 +382,7 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   codes.alloc(ng * k * 4);
   consts.alloc(ng * k * 8);
   ins.alloc(ng * (k + 1) * sizeof(Ins));
-  exe.alloc(2 * ng * (k + 1) * sizeof(Ins));   // two linked copies (grouped interpreter blocks)
+  exe.alloc(kMaxInterpGroups * ng * (k + 1) * sizeof(Ins));   // one linked copy per interpreter genome group
   plen.alloc(ng * 4);
   pnconst.alloc(ng * 4);
   ctab.alloc(ng * k * 8);

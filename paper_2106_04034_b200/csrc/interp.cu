@@ -301,7 +301,10 @@ __device__ __forceinline__ uint4 lds_u128(uint32_t p) {
 }
 
 
-#ifndef GSGP_INTERP_MINB2   // min resident blocks of the grouped launch (register cap)
+// the grouped launch is compiled for a register budget that lets shared
+// memory decide the residency: 4 blocks = 32 warps at 64 registers (a third
+// group per block — 36 warps at 56 registers — measured 5 % slower)
+#ifndef GSGP_INTERP_MINB2
 #define GSGP_INTERP_MINB2 4
 #endif
 // block barrier of one genome group (GROUPS > 1: named barrier 1 + group)
@@ -517,33 +520,33 @@ void launch_cfg(const InterpArgs& a, cudaStream_t s) {
   GSGP_CUDA(cudaGetLastError());
 }
 
-// 128x3 tiles: two genome groups per block share the staged feature tile,
-// so when shared memory (not registers) limits the resident blocks the
-// grouped launch holds more warps per SM (C3: 24 vs 20) — chosen by the
-// occupancy calculator unless GSGP_INTERP_CFG forces a configuration
+// 128x3 tiles: 1 or 2 genome groups per block (cfg 5, 6) share the staged
+// feature tile; when shared memory limits the resident blocks the grouped
+// launch holds more warps per SM.  The occupancy calculator picks the one
+// with more resident warps (ties: one group) unless GSGP_INTERP_CFG forces a
+// configuration (GSGP_INTERP_TRACE=1 prints the numbers).
+template <int MODE, typename TOut, int GROUPS>
+int resident_warps(const InterpArgs& a) {
+  const InterpCfg& c = kCfgs[4 + GROUPS];
+  const size_t sm = cfg_smem(c, a);
+  if (sm > kSmemCap || (GROUPS > 1 && a.exe_gstride <= 0)) return 0;
+  auto k = k_interpret<128, 3, MODE, TOut, true, false, GROUPS>;
+  int b = 0;
+  GSGP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  GSGP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k, 128 * GROUPS, sm));
+  if (getenv("GSGP_INTERP_TRACE")) {
+    cudaFuncAttributes f{};
+    cudaFuncGetAttributes(&f, k);
+    fprintf(stderr, "interp 128x3 x%d groups: %d blocks, %zu B shared, %d regs\n", GROUPS, b, sm, f.numRegs);
+  }
+  return b * 4 * GROUPS;
+}
+
 template <int MODE, typename TOut>
 int grouped_or_single(const InterpArgs& a) {
-  if (a.exe_gstride <= 0 || getenv("GSGP_INTERP_CFG")) return 5;
-  const size_t s1 = cfg_smem(kCfgs[5], a), s2 = cfg_smem(kCfgs[6], a);
-  if (s2 > kSmemCap) return 5;
-  auto k1 = k_interpret<128, 3, MODE, TOut, true, false, 1>;
-  auto k2 = k_interpret<128, 3, MODE, TOut, true, false, 2>;
-  int b1 = 0, b2 = 0;
-  GSGP_CUDA(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1));
-  GSGP_CUDA(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2));
-  GSGP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k1, 128, s1));
-  GSGP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k2, 256, s2));
-  if (getenv("GSGP_INTERP_TRACE")) {
-    cudaFuncAttributes f1{}, f2{};
-    cudaFuncGetAttributes(&f1, k1);
-    cudaFuncGetAttributes(&f2, k2);
-    int z2 = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&z2, k2, 256, 0);
-    fprintf(stderr, "interp cfg: single %d blocks (%zu B, %d regs, %zu static), grouped %d blocks (%zu B, %d regs,"
-            " %zu static, %d blocks without dynamic smem, max threads %d)\n", b1, s1, f1.numRegs,
-            f1.sharedSizeBytes, b2, s2, f2.numRegs, f2.sharedSizeBytes, z2, f2.maxThreadsPerBlock);
-  }
-  return b2 * 8 > b1 * 4 ? 6 : 5;
+  if (getenv("GSGP_INTERP_CFG")) return 5;
+  const int w1 = resident_warps<MODE, TOut, 1>(a), w2 = resident_warps<MODE, TOut, 2>(a);
+  return w2 > w1 ? 6 : 5;
 }
 
 template <int MODE, typename TOut>

@@ -69,12 +69,13 @@ void launch_compile(const uint8_t* tags, const int32_t* codes, const double* con
                     int32_t k, double eps, Program prog, cudaStream_t s);
 
 enum InterpMode : int { INTERP_F64 = 0, INTERP_POP = 1, INTERP_POOL = 2 };
+constexpr int kMaxInterpGroups = 2;   // genome groups per interpreter block (linked program copies)
 
 struct InterpArgs {
   const Ins* code;          // abstract program (count genomes, stride k1)
   Ins* exe;                 // linked copy, rewritten by every launch_interpret
   int64_t exe_gstride;      // elements between the per-group linked copies (0: one copy only;
-                            // grouped configurations need a second copy at exe + exe_gstride)
+                            // grouped configurations need kMaxInterpGroups copies)
   const int32_t* len;
   const int32_t* nconst;
   const double* ctab;       // [count][k1 - 1]
