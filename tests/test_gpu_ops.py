@@ -414,3 +414,20 @@ def test_dataset_split_matches_reference_golden():
         tr, te = G.Dataset(X, np.arange(n, dtype=np.float64)).split(float(frac), int(seed))
         assert np.array_equal(tr.features[:, 0].astype(np.int64), g[f"tr_{n}"]), n
         assert np.array_equal(te.features[:, 0].astype(np.int64), g[f"te_{n}"]), n
+
+
+@pytest.mark.parametrize("count", [1, 2, 3, 5, 17])
+@pytest.mark.parametrize("cfg", ["5", "6"])
+def test_interpreter_genome_groups_with_odd_counts(count, cfg, monkeypatch):
+    """Grouped interpreter blocks (cfg 6: two genome groups of 128 threads
+    per block sharing the feature tile) with genome counts that leave a
+    group idle or uneven: bit-identical to the oracle and to one group."""
+    from oracle import restate as R
+    rng = np.random.default_rng(count)
+    X = rng.uniform(-3, 3, (1000, 6))
+    cfg_run = RunConfig(program_size=63, seed=count)
+    pop = G.create_population(count, cfg_run, 0, 6)
+    ref, _ = R.semantics(pop.tags, pop.codes, pop.consts, X, 1e-6)
+    monkeypatch.setenv("GSGP_INTERP_CFG", cfg)
+    S = G.compute_semantics(pop, X, cfg_run)
+    assert np.array_equal(S.view(np.uint64), ref.view(np.uint64))
