@@ -136,15 +136,18 @@ __device__ __forceinline__ void warp_row_sse_anchored(const double* __restrict__
                                                       int64_t row, int32_t* emax, double* __restrict__ sse) {
   const int lane = threadIdx.x & 31;
   const double* p = part + row * ntiles * 2;
-  // short rows (the launcher sends rows of < 256 units here): every lane
-  // issues its partial loads before the anchor load, so the latencies overlap
+  // groups of 8 strided loads in flight per lane; the first group is issued
+  // before the anchor load, so the latencies overlap
   constexpr int kPer = 8;
-  double2 v[kPer];
+  auto load = [&](int64_t t0, double2* v) {
 #pragma unroll
-  for (int j = 0; j < kPer; ++j) {
-    const int64_t t = lane + 32 * j;
-    v[j] = t < ntiles ? *reinterpret_cast<const double2*>(p + 2 * t) : make_double2(0.0, 0.0);
-  }
+    for (int j = 0; j < kPer; ++j) {
+      const int64_t t = t0 + 32 * j;
+      v[j] = t < ntiles ? *reinterpret_cast<const double2*>(p + 2 * t) : make_double2(0.0, 0.0);
+    }
+  };
+  double2 v[kPer];
+  load(lane, v);
   const int2 A = *reinterpret_cast<const int2*>(emax + 2 * row);
   __syncwarp();
   if (lane == 0) *reinterpret_cast<int2*>(emax + 2 * row) = make_int2(kExpZero, kExpZero);
@@ -152,10 +155,15 @@ __device__ __forceinline__ void warp_row_sse_anchored(const double* __restrict__
 #pragma unroll
   for (int d = 0; d < 2 * kLimbs; ++d) L[d] = 0;
   const bool fx = A.x < kExpInf, fz = A.y < kExpInf;
+  for (int64_t t0 = lane;;) {
 #pragma unroll
-  for (int j = 0; j < kPer; ++j) {
-    if (fx) canon_add(v[j].x, A.x, L);
-    if (fz) canon_add(v[j].y, A.y, L + kLimbs);
+    for (int j = 0; j < kPer; ++j) {
+      if (fx) canon_add(v[j].x, A.x, L);
+      if (fz) canon_add(v[j].y, A.y, L + kLimbs);
+    }
+    t0 += 32 * kPer;
+    if (t0 - lane >= ntiles) break;
+    load(t0, v);
   }
 #pragma unroll
   for (int d = 0; d < 2 * kLimbs; ++d)
@@ -588,7 +596,8 @@ void launch_reduce_survive(const double* part, int64_t ntiles, int32_t* emax, do
                            const SurviveArgs& a, unsigned int* done, cudaStream_t s) {
   if (ntiles == 1)     // emax is not used (the generation launch leaves it untouched)
     k_reduce_survive_single<<<(unsigned)((2 * a.m + 255) / 256), 256, 0, s>>>(part, sse, a, done);
-  else if (ntiles > 256)   // long rows (C3 ~3000 tiles): a block per row; else a warp (8 loads per lane)
+  else if (ntiles > 1024)  // long rows (C3 ~3000 units): a block per row; else a warp per row
+                           // (C2 31, C4 306, C5 611 units: 8 loads per lane in flight)
     k_reduce_survive_wide<<<(unsigned)a.m, 256, 0, s>>>(part, ntiles, emax, sse, a, done);
   else
     k_reduce_survive<<<(unsigned)((a.m + 7) / 8), 256, 0, s>>>(part, ntiles, emax, sse, a, done);
