@@ -208,7 +208,7 @@ struct InterpCfg {
 };
 constexpr InterpCfg kCfgs[] = {{128, 4, true, false}, {64, 8, true, false}, {128, 4, false, false},
                                {128, 2, true, false}, {128, 1, false, true}, {128, 3, true, false},
-                               {128, 3, true, false, 2}};
+                               {128, 3, true, false, 2}, {128, 4, true, false, 2}};
 constexpr int kNumCfgs = sizeof(kCfgs) / sizeof(kCfgs[0]);
 constexpr size_t kSmemCap = 200 * 1024;
 
@@ -235,6 +235,12 @@ int choose_cfg(const InterpArgs& a) {
   if (forced >= 0 && forced < kNumCfgs && cfg_smem(kCfgs[forced], a) <= kSmemCap &&
       (kCfgs[forced].groups == 1 || a.exe_gstride > 0))
     return forced;
+  // two genome groups of 128 x 4 per block (cfg 7, compiled for 3 resident
+  // blocks = 24 warps) when shared memory keeps 3 of them per SM: measured
+  // 2.8 % faster at C3 than 128 x 3 groups with 32 warps (more cases per
+  // dispatched instruction); the decision uses only shared memory, so it is
+  // the same for every kernel instance and every rank
+  if (a.exe_gstride > 0 && 3 * (cfg_smem(kCfgs[7], a) + 2048) <= 228 * 1024) return 7;
   // features in shared memory while the tile keeps >= 3 blocks per SM; the
   // 384-case tile (128 x 3) fits 5 blocks (20 warps) where 128 x 4 fits 4:
   // measured 1-4 % faster (profiles/r01/README.md)
@@ -319,7 +325,7 @@ __device__ __forceinline__ void group_sync(int grp) {
 // and constant rows (grp_bytes apart) and program slot (prog_bytes apart),
 // linked for it by k_link (copy `grp` of the linked programs)
 template <int NT, int CPT, int MODE, typename TOut, bool kXSmem, bool kLean, int GROUPS>
-__global__ void __launch_bounds__(NT * GROUPS, GROUPS == 2 ? GSGP_INTERP_MINB2 : 1) k_interpret(InterpArgs a, int64_t gpb,
+__global__ void __launch_bounds__(NT * GROUPS, GROUPS == 2 ? (CPT == 3 ? GSGP_INTERP_MINB2 : 3) : 1) k_interpret(InterpArgs a, int64_t gpb,
                                                            uint32_t stack_off, uint32_t crow_off,
                                                            uint32_t prog_off, uint32_t grp_bytes,
                                                            uint32_t prog_bytes) {
@@ -560,6 +566,7 @@ void launch_mode(const InterpArgs& a, cudaStream_t s) {
     case 3: launch_cfg<128, 2, MODE, TOut, true>(a, s); break;
     case 5: launch_cfg<128, 3, MODE, TOut, true>(a, s); break;
     case 6: launch_cfg<128, 3, MODE, TOut, true, false, 2>(a, s); break;
+    case 7: launch_cfg<128, 4, MODE, TOut, true, false, 2>(a, s); break;
     default: launch_cfg<128, 1, MODE, TOut, false, true>(a, s); break;
   }
 }

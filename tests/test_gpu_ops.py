@@ -394,7 +394,7 @@ def test_interpreter_division_fast_path_near_halfway_quotients():
     ref, _ = R.semantics(tags, codes, consts, X, 1e-6)
     pop = Population(tags, codes, consts)
     import os
-    for cfg in ("0", "1", "2", "3", "4", "5", "6"):
+    for cfg in ("0", "1", "2", "3", "4", "5", "6", "7"):
         os.environ["GSGP_INTERP_CFG"] = cfg
         try:
             S = G.compute_semantics(pop, X, RunConfig(program_size=k))
@@ -417,7 +417,7 @@ def test_dataset_split_matches_reference_golden():
 
 
 @pytest.mark.parametrize("count", [1, 2, 3, 5, 17])
-@pytest.mark.parametrize("cfg", ["5", "6"])
+@pytest.mark.parametrize("cfg", ["5", "6", "7"])
 def test_interpreter_genome_groups_with_odd_counts(count, cfg, monkeypatch):
     """Grouped interpreter blocks (cfg 6: two genome groups of 128 threads
     per block sharing the feature tile) with genome counts that leave a
