@@ -132,13 +132,14 @@ __device__ __forceinline__ void warp_row_sse(const double* __restrict__ part, in
 
 // the fused generation tail: anchors come from the GSM launch (emax), which
 // is reset to kExpZero for the next generation once read
+template <int kPer>
 __device__ __forceinline__ void warp_row_sse_anchored(const double* __restrict__ part, int64_t ntiles,
                                                       int64_t row, int32_t* emax, double* __restrict__ sse) {
   const int lane = threadIdx.x & 31;
   const double* p = part + row * ntiles * 2;
-  // groups of 8 strided loads in flight per lane; the first group is issued
-  // before the anchor load, so the latencies overlap
-  constexpr int kPer = 8;
+  // groups of kPer strided loads in flight per lane (1 for rows of <= 32
+  // units, else 8); the first group is issued before the anchor load, so the
+  // latencies overlap
   auto load = [&](int64_t t0, double2* v) {
 #pragma unroll
     for (int j = 0; j < kPer; ++j) {
@@ -404,12 +405,13 @@ __global__ void __launch_bounds__(1024) k_survive(SurviveArgs a) { survive_block
 
 // Canonical SSE of every row (one warp per row, warp_row_sse above) fused
 // with survival: the last block to finish runs survive_block.
+template <int kPer>
 __global__ void __launch_bounds__(256) k_reduce_survive(const double* __restrict__ part, int64_t ntiles,
                                                         int32_t* emax, double* __restrict__ sse,
                                                         SurviveArgs a, unsigned int* done) {
   __shared__ int last;
   const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (row < a.m) warp_row_sse_anchored(part, ntiles, row, emax, sse);
+  if (row < a.m) warp_row_sse_anchored<kPer>(part, ntiles, row, emax, sse);
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
@@ -600,7 +602,8 @@ void launch_reduce_survive(const double* part, int64_t ntiles, int32_t* emax, do
                            // (C2 31, C4 306, C5 611 units: 8 loads per lane in flight)
     k_reduce_survive_wide<<<(unsigned)a.m, 256, 0, s>>>(part, ntiles, emax, sse, a, done);
   else
-    k_reduce_survive<<<(unsigned)((a.m + 7) / 8), 256, 0, s>>>(part, ntiles, emax, sse, a, done);
+    (ntiles <= 32 ? k_reduce_survive<1> : k_reduce_survive<8>)<<<(unsigned)((a.m + 7) / 8), 256, 0, s>>>(
+        part, ntiles, emax, sse, a, done);
   check_launch();
 }
 
