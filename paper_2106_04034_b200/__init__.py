@@ -8,9 +8,7 @@ through `libgsgp_b200.so`.  Importing the package does not touch the GPU;
 the first compute call loads the library and fails loudly if it is missing.
 """
 
-from .backend import (
-    BackendDescriptor, CudaBackend, SequentialBackend, ThreadBackend, choose_chunk, get_backend,
-)
+from .backend import BackendDescriptor, get_backend
 from .core import (
     BACKENDS, WORST_FITNESS, Chromosome, ConfigError, Dataset, DatasetFormatError, EliteRecord,
     FunctionOp, Gene, GeneTag, GsgpError, LineageEntry, LineageError, LineageLog, MutationPlan,

@@ -92,20 +92,20 @@ constexpr int kTileBytes = GSGP_GSM_TILE;
 // case tiles in lockstep and each pool tile is fetched from HBM once, then
 // re-served from L2 to every row that references it (pool copies: L2
 // evict_last; parent: evict_first; offspring stores: streaming).
-//   warp 8  producer: claims batches of units, the warp's lanes draw the
-//           rows' mutation plans (u, v, ms) from the counter RNG in
-//           parallel, and one lane issues 3 cp.async.bulk
-//           copies (parent row tile, pool[u] tile, pool[v] tile) into a
-//           kStages-deep shared-memory ring; completion = mbarrier
-//           transaction count.
-//   warps 0-7 consumers: copy the unit out of shared memory into registers,
-//           release the stage at once (so the producer refills it while
-//           they compute), mutate, store the offspring with 128-bit
+//   warp W  producer (W = kConsumerWarps, 16 by default): claims batches
+//           of units, the warp's lanes draw the rows' mutation plans
+//           (u, v, ms) from the counter RNG in parallel, and one lane issues
+//           3 cp.async.bulk copies (parent row tile, pool[u] tile, pool[v]
+//           tile) into a kStages-deep shared-memory ring; completion =
+//           mbarrier transaction count.
+//   warps 0..W-1 consumers: copy the unit out of shared memory into
+//           registers, release the stage at once (so the producer refills it
+//           while they compute), mutate, store the offspring with 128-bit
 //           streaming stores, save the best parent row, and accumulate the
 //           fp64 SSE against the target, which each thread keeps in
 //           registers for as long as the CTA stays on the same case tile.
-//   warp 9  finalizer (one lane): folds the 8 per-warp SSE partials of each
-//           unit (fixed warp order) into part[i][t], decoupled from the
+//   warp W+1 finalizer (one lane): folds the W per-warp SSE partials of
+//           each unit (fixed warp order) into part[i][t], decoupled from the
 //           consumers through a small mbarrier ring.
 // ===================================================================
 constexpr int kStages = GSGP_GSM_STAGES;
@@ -514,7 +514,10 @@ void launch_gsm_mode(const GsmArgs& a, bool f64, int mode, cudaStream_t s) {
   // consecutive rows of one tile (C3 0.91 -> 0.97 of peak at 16), but the
   // last claims of a small launch must still balance across CTAs, so keep
   // >= 48 claims per CTA (profiles/r01/README.md, batch A/B)
-  static const int forced = getenv("GSGP_GSM_BATCH") ? atoi(getenv("GSGP_GSM_BATCH")) : 0;
+  // GSGP_GSM_BATCH (tests, A/B) is read at every launch so one process can
+  // exercise several claim sizes
+  const char* fb = getenv("GSGP_GSM_BATCH");
+  const int forced = fb ? atoi(fb) : 0;
   int batch = 2;
   while (batch < 16 && nunits / ((int64_t)grid * 2 * batch) >= 48) batch *= 2;
   if (forced > 0) batch = forced < 32 ? forced : 32;   // one unit per producer lane

@@ -576,7 +576,7 @@ void launch_mode(const InterpArgs& a, cudaStream_t s) {
 void launch_compile(const uint8_t* tags, const int32_t* codes, const double* consts, int64_t count,
                     int32_t k, double eps, Program prog, cudaStream_t s) {
   if (count <= 0) return;
-  GSGP_CUDA(cudaMemsetAsync(prog.maxima, 0, 2 * sizeof(int32_t), s));
+  GSGP_CUDA(cudaMemsetAsync(prog.maxima, 0, 3 * sizeof(int32_t), s));   // all three maxima
   k_compile<<<(unsigned)((count + 63) / 64), 64, 0, s>>>(tags, codes, consts, count, k, eps, prog);
   GSGP_CUDA(cudaGetLastError());
 }

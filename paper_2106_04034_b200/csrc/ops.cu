@@ -74,20 +74,6 @@ __global__ void k_plan(PlanParams p, int64_t gen, const int64_t* gen_ptr, int64_
 }
 
 // ------------------------------------------------------- reductions
-// Block-wide fp64 sum with a fixed order: per-warp butterfly, then warps in
-// index order.  Every thread gets the result.
-__device__ double block_sum(double v, double* sh) {
-  v = warp_sum(v);
-  int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __syncthreads();
-  if (lane == 0) sh[w] = v;
-  __syncthreads();
-  double t = 0.0;
-  int nw = blockDim.x >> 5;
-  for (int i = 0; i < nw; ++i) t = __dadd_rn(t, sh[i]);
-  return t;
-}
-
 // Canonical SSE of part[row][tile][2] (common.cuh): one warp per row.  The
 // anchors are the exact max partial exponents; the digit sums are exact.
 __device__ __forceinline__ int2 warp_row_exp(const double* __restrict__ p, int64_t ntiles, int lane) {
@@ -276,17 +262,36 @@ __global__ void k_canon_finish(const int32_t* __restrict__ emax, const unsigned 
 }
 
 // fp64 RMSE of each row (operator API, fitness.py:28-51)
-__global__ void k_row_rmse(const double* __restrict__ S, const double* __restrict__ y, int64_t n,
-                           double* out) {
-  __shared__ double sh[32];
-  const double* row = S + blockIdx.x * n;
-  double a = 0.0;
-  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
-    double d = __dsub_rn(row[j], y[j]);
-    a = __dadd_rn(a, __dmul_rn(d, d));
+// Operator RMSE (gsgp/fitness.py:11-51): the reference accumulates every row
+// strictly left to right (np.cumsum(diff * diff)[-1]), and documents the
+// result as bitwise identical across backends, so the operator keeps that
+// order: one thread per row adds its squares sequentially.  A block owns 32
+// rows; its 256 threads stage a 32 x 64 tile of squared differences in shared
+// memory with coalesced loads, then warp 0 folds the tile into the 32 running
+// sums in column order.  (The engine's fitness uses the canonical sum
+// instead — common.cuh — which is order-free across tiles and ranks.)
+constexpr int kRmseRows = 32, kRmseCols = 64;
+__global__ void __launch_bounds__(256) k_row_rmse(const double* __restrict__ S, const double* __restrict__ y,
+                                                  int64_t m, int64_t n, double* out) {
+  __shared__ double sq[kRmseRows][kRmseCols + 1];
+  const int64_t r0 = (int64_t)blockIdx.x * kRmseRows;
+  const int t = threadIdx.x;
+  double acc = 0.0;
+  for (int64_t c0 = 0; c0 < n; c0 += kRmseCols) {
+    const int64_t w = n - c0 < kRmseCols ? n - c0 : kRmseCols;
+    for (int e = t; e < kRmseRows * kRmseCols; e += 256) {
+      const int rr = e / kRmseCols, cc = e % kRmseCols;
+      if (r0 + rr < m && cc < w) {
+        const double d = __dsub_rn(S[(r0 + rr) * n + c0 + cc], y[c0 + cc]);
+        sq[rr][cc] = __dmul_rn(d, d);
+      }
+    }
+    __syncthreads();
+    if (t < kRmseRows && r0 + t < m)
+      for (int cc = 0; cc < w; ++cc) acc = __dadd_rn(acc, sq[t][cc]);
+    __syncthreads();
   }
-  a = block_sum(a, sh);
-  if (threadIdx.x == 0) out[blockIdx.x] = rmse_of(a, (double)n);
+  if (t < kRmseRows && r0 + t < m) out[r0 + t] = rmse_of(acc, (double)n);
 }
 
 // ---------------------------------------------------------- arg-min/max
@@ -590,7 +595,7 @@ void launch_reduce_partials(const double* part, int64_t rows, int64_t ntiles, do
 void launch_row_rmse(const double* S, const double* y, int64_t m, int64_t n, double* out,
                      cudaStream_t s) {
   if (m <= 0) return;
-  k_row_rmse<<<(unsigned)m, 256, 0, s>>>(S, y, n, out);
+  k_row_rmse<<<(unsigned)((m + kRmseRows - 1) / kRmseRows), 256, 0, s>>>(S, y, m, n, out);
   check_launch();
 }
 

@@ -176,7 +176,13 @@ def interpret(chromosome: Chromosome, case_features, eps: float) -> float:
 
 # ---------------------------------------------------------------- fitness.py
 def compute_fitness(semantics: np.ndarray, target, backend=None) -> np.ndarray:
-    """gsgp/fitness.py:28-51: per-row RMSE, non-finite -> +inf."""
+    """gsgp/fitness.py:28-51: per-row RMSE, non-finite -> +inf.
+
+    Bitwise the reference's value: the device kernel adds each row's squared
+    differences strictly left to right, the order of the reference's
+    np.cumsum.  (The engine's in-loop fitness differs from this operator in
+    the last bits: it is the canonical tile sum of DESIGN.md §4, which is
+    independent of how the cases are split across tiles and GPUs.)"""
     S = _f64(semantics)
     y = _f64(target)
     if S.ndim != 2 or S.shape[1] != y.shape[0]:
@@ -187,7 +193,7 @@ def compute_fitness(semantics: np.ndarray, target, backend=None) -> np.ndarray:
 
 
 def rmse(row, target) -> float:
-    """gsgp/fitness.py:11-25."""
+    """gsgp/fitness.py:11-25 (bitwise; see compute_fitness)."""
     a = _f64(row)
     b = _f64(target)
     if a.shape != b.shape or a.ndim != 1 or a.shape[0] == 0:

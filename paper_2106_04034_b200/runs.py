@@ -18,7 +18,7 @@ from __future__ import annotations
 import os
 from dataclasses import dataclass
 
-from .core import ConfigError, RunConfig
+from .core import ConfigError, GsgpError, RunConfig
 
 
 def run_seeds(cfg: RunConfig) -> list[int]:
@@ -83,14 +83,25 @@ def run_many(cfg: RunConfig, train, test, *, group=None, gather: str = "results"
     seeds = run_seeds(cfg)
     mine = assign_runs(cfg.runs, world, rank)
     out: list = [None] * cfg.runs
+    failure = None
     for i in mine:
-        res = run_fn(cfg.with_seed(seeds[i]), train, test, **engine_kw)
-        if on_result is not None:
-            on_result(i, res)
+        try:
+            res = run_fn(cfg.with_seed(seeds[i]), train, test, **engine_kw)
+            if on_result is not None:
+                on_result(i, res)
+        except (GsgpError, OSError) as exc:
+            # a failing rank still reaches the gather below, so the other
+            # ranks never block in it until the process-group timeout
+            if world == 1 or gather == "none":
+                raise
+            failure = (i, rank, f"{type(exc).__name__}: {exc}")
+            break
         out[i] = res
     if world == 1 or gather == "none":
         return out
-    if gather == "summary":
+    if failure is not None:
+        payload = {"__failure__": failure}
+    elif gather == "summary":
         payload = {i: RunSummary(i, seeds[i], list(map(float, out[i].train_fitness)),
                                  list(map(float, out[i].test_fitness)), int(out[i].overflow_replacements),
                                  out[i].timings, rank) for i in mine}
@@ -98,7 +109,13 @@ def run_many(cfg: RunConfig, train, test, *, group=None, gather: str = "results"
         payload = {i: out[i] for i in mine}
     parts = [None] * world if rank == 0 else None
     td.gather_object(payload, parts, dst=0, group=group)
+    if failure is not None:
+        raise GsgpError(f"run {failure[0]} failed on rank {failure[1]}: {failure[2]}")
     if rank == 0:
+        failed = [p["__failure__"] for p in parts if "__failure__" in p]
+        if failed:
+            i, r, msg = failed[0]
+            raise GsgpError(f"run {i} failed on rank {r}: {msg}")
         for part in parts:
             for i, v in part.items():
                 if out[i] is None:

@@ -232,9 +232,24 @@ def test_fitness_against_reference_sequential_sums():
     ref = g["fit_out"]
     assert got[7] == ref[7] == math.inf
     assert got[5] == 0.0
-    np.testing.assert_allclose(got, ref, rtol=1e-12)
-    assert G.rmse([0.0, 0.0], [3.0, 4.0]) == pytest.approx(3.5355339059327378, abs=1e-15)
+    np.testing.assert_array_equal(got, ref)       # same left-to-right order: bitwise
+    assert G.rmse([0.0, 0.0], [3.0, 4.0]) == 3.5355339059327378
     assert G.rmse([1e200, 0.0], [-1e200, 0.0]) == math.inf
+
+
+@pytest.mark.parametrize("m,n", [(1, 1), (3, 63), (31, 64), (33, 65), (70, 1000), (5, 100_003)])
+def test_fitness_is_bitwise_numpy_cumsum_order(m, n):
+    """gsgp/fitness.py:43-48: np.cumsum(diff * diff, axis=1)[:, -1] is a
+    strictly sequential sum; the operator kernel keeps that order, so the
+    RMSE is bitwise the reference's for every shape (rows straddling the
+    kernel's 32-row blocks and 64-column tiles)."""
+    rng = np.random.default_rng(m * 1000 + n)
+    S = rng.lognormal(0, 4, (m, n)) * rng.choice([-1.0, 1.0], (m, n))
+    y = rng.normal(0, 3, n)
+    with np.errstate(all="ignore"):
+        want = np.sqrt(np.cumsum((S - y) * (S - y), axis=1)[:, -1] / n)
+    want = np.where(np.isfinite(want), want, math.inf)
+    np.testing.assert_array_equal(G.compute_fitness(S, y), want)
 
 
 # ------------------------------------------------------------------ plan

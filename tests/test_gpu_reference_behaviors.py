@@ -38,7 +38,7 @@ def test_replay_reproduces_live_elite_bitwise_at_scale():
     replayed = G.replay_lineage(res.lineage, *_initial(cfg, train), cfg)
     assert np.array_equal(replayed, res.elite_train_semantics)
     # the operator rmse sums sequentially like numpy's cumsum; the engine's
-    # fitness sums in fixed case tiles: equal to the last ulps
+    # fitness is the canonical tile sum: equal to the last ulps
     assert G.rmse(replayed, train.target) == pytest.approx(res.train_fitness[-1], rel=1e-14)
 
 

@@ -96,3 +96,45 @@ def test_replicas_over_gloo_ranks_match_sequential_runs(world, gather):
                 assert summary[i] == (list(map(float, s.train_fitness)), list(map(float, s.test_fitness)))
         else:
             assert [i for i, v in enumerate(summary) if v is not None] == ran
+
+
+def _failing_run(cfg: RunConfig, train, test, **kw):
+    if cfg.seed == run_seeds(RunConfig(**CFG))[1]:      # run 1 (rank 1) fails
+        from paper_2106_04034_b200.core import GsgpError
+        raise GsgpError("injected failure")
+    return _oracle_run(cfg, train, test, **kw)
+
+
+def _fail_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    td.init_process_group("gloo", rank=rank, world_size=world, timeout=__import__("datetime").timedelta(seconds=60))
+    try:
+        from paper_2106_04034_b200.core import GsgpError
+        from paper_2106_04034_b200.runs import run_many
+        Xtr, ytr, Xte, yte = _data()
+        try:
+            run_many(RunConfig(**CFG), (Xtr, ytr), (Xte, yte), gather="summary", run_fn=_failing_run)
+            q.put((rank, "ok"))
+        except GsgpError as exc:
+            q.put((rank, str(exc)))
+    finally:
+        td.destroy_process_group()
+
+
+def test_replica_failure_reaches_every_rank_without_hanging():
+    """A run that raises on one rank is reported as GsgpError on that rank and
+    on rank 0 (the CLI's clean 'error:' exit) instead of leaving the other
+    ranks blocked in the gather until the process-group timeout."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fail_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert "injected failure" in got[0] and "rank 1" in got[0]
+    assert "injected failure" in got[1]
