@@ -45,7 +45,7 @@ typedef struct gsgp_config {
   int32_t gsm_sign;              /* 0 "minus", 1 "plus" */
   double mutation_step;          /* constant step when !mutation_step_uniform */
   double division_eps;
-  int32_t storage_f64;           /* 0: fp32 semantic storage (default); 1: fp64 */
+  int32_t storage_f64;           /* 0: fp32 semantic storage (default; see storage_f64_used); 1: fp64 */
   int32_t use_graph;             /* 1: replay one captured generation as a CUDA graph */
   int32_t time_kernels;          /* 1: CUDA events around every GSM launch */
   int32_t virtual_shards;        /* case shards per process on its device (>= 1) */
@@ -78,6 +78,11 @@ typedef struct gsgp_outputs {
                                     16 genome compile, 17 device allocation + clears (host
                                     clock), 18 / 19 total compiled instructions (counts, not ms)
                                     of the population / random-tree programs */
+  int64_t storage_f64_used;      /* out: 1 if the semantics were stored in fp64 (requested, or
+                                    forced by a constant mutation step large enough to leave
+                                    fp32 range: step * (1 minus | 2 plus) * g >= 2^70) */
+  int64_t interp_info[4];        /* out: interpreter launch configuration, and the compiled
+                                    programs' max spill depth, constants, instructions */
 } gsgp_outputs;
 
 const char* gsgp_version(void);

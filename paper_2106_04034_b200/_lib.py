@@ -60,6 +60,8 @@ class GsgpOutputs(C.Structure):
         ("overflow", C.c_int64),
         ("shard_train_lo", C.c_int64), ("shard_train_hi", C.c_int64),
         ("stage_ms", C.c_double * 20),
+        ("storage_f64_used", C.c_int64),
+        ("interp_info", C.c_int64 * 4),
     ]
 
 

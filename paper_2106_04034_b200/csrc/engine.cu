@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -333,7 +334,19 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   GSGP_REQUIRE(cfg->p_function >= 0 && cfg->p_feature >= 0 && cfg->p_constant >= 0 && total > 0,
                "gene probabilities must be non-negative with positive sum");
   GSGP_REQUIRE(cfg->division_eps > 0, "division_eps must be > 0");
-  const bool f64 = cfg->storage_f64 != 0;
+  GSGP_REQUIRE(cfg->mutation_step_uniform || (std::isfinite(cfg->mutation_step) && cfg->mutation_step > 0),
+               "constant mutation_step must be finite and > 0");
+  // fp32 storage is only taken when no stored value can leave fp32 range or
+  // drift far enough to move an fp32-overflow row's fitness:
+  // per generation |t| <= step * (1 or 2), so a cumulative drift below 2^70
+  // keeps every finite fp32 value finite (a step < 2^103 cannot round past
+  // FLT_MAX) and leaves the squares of overflow rows absorbed.  Larger
+  // constant steps (gsgp/core.py:332-336 allows any finite step) run in fp64.
+  const double step_bound = (cfg->mutation_step_uniform ? 1.0 : cfg->mutation_step) *
+                            (cfg->gsm_sign ? 2.0 : 1.0) * (double)(g > 0 ? g : 1);
+  const bool f64 = cfg->storage_f64 != 0 || !(step_bound < 0x1p70);
+  out->storage_f64_used = f64 ? 1 : 0;
+  for (int q = 0; q < 4; ++q) out->interp_info[q] = -1;
   const size_t esz = f64 ? 8 : 4;
   const int G = cfg->virtual_shards < 1 ? 1 : cfg->virtual_shards;
   GSGP_REQUIRE(G <= 16, "at most 16 virtual shards");
@@ -489,6 +502,8 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
     ia.nonfinite = nonfinite.as<unsigned long long>();
     int itile = 1;
     interp_tiles(ia, &itile);
+    out->interp_info[0] = interp_config(ia);
+    for (int q = 0; q < 3; ++q) out->interp_info[1 + q] = maxima[q];
     // test cases start on an interpreter tile (stacked index te_q), so no
     // tile mixes train and test cases: canonical partials (see shard_range)
     ia.te_q = (p->ntr + itile - 1) / itile * itile;

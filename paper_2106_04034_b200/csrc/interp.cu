@@ -581,6 +581,8 @@ void launch_compile(const uint8_t* tags, const int32_t* codes, const double* con
   GSGP_CUDA(cudaGetLastError());
 }
 
+int interp_config(const InterpArgs& a) { return choose_cfg(a); }
+
 int64_t interp_tiles(const InterpArgs& a, int* tile_out) {
   const InterpCfg c = kCfgs[choose_cfg(a)];
   const int64_t tile = (int64_t)c.nt * c.cpt;

@@ -107,6 +107,9 @@ struct InterpArgs {
 };
 // case tiles over all te_q + nte stacked cases (the part[] row stride) and the tile size
 int64_t interp_tiles(const InterpArgs& a, int* tile_out);
+// launch configuration index the interpreter takes for these arguments (a
+// function of shared memory only: the same on every rank and every run)
+int interp_config(const InterpArgs& a);
 void launch_interpret(const InterpArgs& a, int mode, cudaStream_t s);
 
 // ------------------------------------------------------------ storage rows

@@ -128,7 +128,11 @@ def run_evolution(cfg: RunConfig, train: Dataset, test: Dataset, *, storage: str
                           "interpret_pool": st[14], "initial_sse": st[15], "compile": st[16],
                           "alloc": st[17]},
               "program_instructions": {"population": int(st[18]), "pool": int(st[19])},
-              "storage": storage}
+              "storage": "fp64" if out.storage_f64_used else "fp32",
+              "storage_requested": storage,
+              "interpreter": {"config": int(out.interp_info[0]), "max_spill_depth": int(out.interp_info[1]),
+                              "max_constants": int(out.interp_info[2]),
+                              "max_instructions": int(out.interp_info[3])}}
     return RunResult(
         config=cfg, train_fitness=a["train_trace"], test_fitness=a["test_trace"], lineage=log,
         timings=timings, elite_slot=int(log.final_elite().slot),

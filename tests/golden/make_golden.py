@@ -252,11 +252,20 @@ RUNS = {
     # 5 initial rows exceed FLT_MAX: exercises the engine's fp32-overflow slots
     "wide": (dict(population_size=1024, random_trees=64, program_size=1024, generations=40, seed=2),
              (300, 5, 1), (100, 2), "bench"),
+    # constant steps past fp32 range (gsgp/core.py:332-336 accepts any finite
+    # positive step): the reference stays finite in fp64 where an fp32 store
+    # would overflow; the engine must not take the fp32 path for these
+    "hugestep": (dict(population_size=16, random_trees=8, program_size=31, generations=20, seed=41,
+                      mutation_step=1e38, gsm_sign="plus"), (40, 3, 13), (12, 14), "toy"),
+    "infstep": (dict(population_size=12, random_trees=6, program_size=21, generations=8, seed=43,
+                     mutation_step=1e39, gsm_sign="plus"), (30, 3, 15), (10, 16), "toy"),
 }
 
 
-def gen_runs():
+def gen_runs(names=None):
     for name, (kw, (ntr, l, s1), (nte, s2), kind) in RUNS.items():
+        if names and name not in names:
+            continue
         cfg = RunConfig(backend="sequential", **kw)
         if kind == "toy":
             tr, te = toy_dataset(ntr, l, seed=s1), toy_dataset(nte, l, seed=s2)
@@ -283,6 +292,52 @@ def gen_runs():
             blobs["ms"] = np.array([e.plan.ms for e in log.entries]).reshape(cfg.generations, -1)
         np.savez_compressed(OUT / f"run_{name}.npz", **blobs)
         print(f"run {name}: {dt:.1f}s, parent elites {int((src == 0).sum())}/{len(src)}")
+
+
+# Headline-shape runs (VERDICT r01 "Missing" #1): the shapes whose generation
+# kernel and SSE reduction configurations the benchmarks run.  Units per row
+# (4096-case fp32 tiles): c2 = 31 (C2 itself), mid = 123 (33..1024: the
+# warp-per-row reduce), long = 1124 (> 1024: the block-per-row reduce of C3).
+# The data is NOT stored: tests regenerate it with make_benchmark_dataset
+# (bit-exact with the reference, pinned by ops.npz bench_* vectors).  Stored:
+# traces, elite records, plans (uint16) and a strided sample (~20k values) of
+# the final elite's train semantics.
+BIG_RUNS = {
+    "c2": (dict(population_size=1024, random_trees=1024, program_size=1024, generations=5, seed=1),
+           (100_000, 8, 1), (25_000, 2)),
+    "mid": (dict(population_size=64, random_trees=32, program_size=63, generations=4, seed=17),
+            (400_000, 6, 3), (100_000, 4)),
+    "long": (dict(population_size=8, random_trees=8, program_size=31, generations=3, seed=23),
+             (4_300_000, 4, 5), (300_000, 6)),
+}
+
+
+def gen_big_runs(names=None):
+    for name, (kw, (ntr, l, s1), (nte, s2)) in BIG_RUNS.items():
+        if names and name not in names:
+            continue
+        cfg = RunConfig(backend="threads", **kw)
+        tr, te = make_benchmark_dataset(ntr, l, seed=s1), make_benchmark_dataset(nte, l, seed=s2)
+        t0 = time.perf_counter()
+        res = run_evolution(cfg, tr, te)
+        dt = time.perf_counter() - t0
+        log = res.lineage
+        blobs = dict(
+            train=res.train_fitness, test=res.test_fitness,
+            src=np.array([0 if e.elite.source == "parent" else 1 for e in log.entries], np.int8),
+            idx=np.array([e.elite.index for e in log.entries], np.int64),
+            slot=np.array([e.elite.slot for e in log.entries], np.int64),
+            fit=np.array([e.elite.fitness for e in log.entries]),
+            init=np.array([log.initial_elite.index]), init_fit=np.array([log.initial_elite.fitness]),
+            u=np.array([e.plan.u for e in log.entries], np.uint16),
+            v=np.array([e.plan.v for e in log.entries], np.uint16),
+            ms=np.array([e.plan.ms for e in log.entries]),
+            elite_sem_sample=res.elite_train_semantics[::max(7, ntr // 20000)].copy(),
+            sample_stride=np.array([max(7, ntr // 20000)]),
+            slot_final=np.array([res.elite_slot]), overflow=np.array([res.overflow_replacements]),
+            data=np.array([ntr, l, s1, nte, s2], np.int64), cfg=np.array([repr(kw)]))
+        np.savez_compressed(OUT / f"big_{name}.npz", **blobs)
+        print(f"big run {name}: {dt:.1f}s, parent elites {int((blobs['src'] == 0).sum())}/{len(log.entries)}")
 
 
 def gen_cli():
@@ -319,6 +374,12 @@ def gen_split():
 
 
 if __name__ == "__main__":
+    if sys.argv[1:2] == ["big"]:          # python make_golden.py big [names...]
+        gen_big_runs(sys.argv[2:])
+        sys.exit(0)
+    if sys.argv[1:2] == ["runs"]:         # python make_golden.py runs [names...]
+        gen_runs(sys.argv[2:])
+        sys.exit(0)
     gen_split()
     gen_rng()
     gen_population()
@@ -326,4 +387,5 @@ if __name__ == "__main__":
     gen_ops()
     gen_runs()
     gen_cli()
+    gen_big_runs()
     print("golden fixtures written to", OUT)

@@ -59,3 +59,37 @@ def test_gsm_step32_rounding_order():
     t = np.float32(np.float32(0.8) - np.float32(0.3)) * np.float32(0.1)
     assert o[0, 0] == np.float32(np.float32(1.0) + np.float32(t))
     assert abs(float(o[0, 0]) - 1.05) < 1e-6
+
+
+@pytest.mark.parametrize("name", ["hugestep", "infstep"])
+def test_fp32_storage_is_unsafe_for_huge_constant_steps(name):
+    """gsgp/core.py:332-336 accepts any finite positive constant step.  With
+    steps near FLT_MAX (1e38 plus-sign; 1e39 > FLT_MAX) plain fp32 storage
+    overflows where the fp64 reference stays finite, and the survival slots
+    diverge — which is why the engine stores such runs in fp64 (engine.cu:
+    step * (1|2) * g >= 2^70).  The fp64 restatement is the reference."""
+    g = golden(f"run_{name}")
+    cfg = R.Cfg(**ast.literal_eval(str(g["cfg"][0])))
+    with np.errstate(all="ignore"):
+        out = engine32.run32(cfg, g["Xtr"], g["ytr"], g["Xte"], g["yte"])
+    assert [e[2] for e in out["elite"]] != g["slot"].tolist()
+    ref = R.run(cfg, g["Xtr"], g["ytr"], g["Xte"], g["yte"])
+    assert [e[2] for e in ref["elite"]] == g["slot"].tolist()
+
+
+@pytest.mark.parametrize("name", ["mid", "long"])
+def test_fp32_storage_reproduces_reference_at_headline_shapes(name):
+    """The fp32 design against the reference-generated headline-shape goldens
+    (make_golden.py BIG_RUNS; data regenerated from the benchmark seeds)."""
+    g = golden(f"big_{name}")
+    ntr, l, s1, nte, s2 = (int(x) for x in g["data"])
+    Xtr, ytr = R.benchmark_dataset(ntr, l, s1)
+    Xte, yte = R.benchmark_dataset(nte, l, s2)
+    out = engine32.run32(R.Cfg(**ast.literal_eval(str(g["cfg"][0]))), Xtr, ytr, Xte, yte)
+    assert [e[2] for e in out["elite"]] == g["slot"].tolist()
+    assert [e[1] for e in out["elite"]] == g["idx"].tolist()
+    np.testing.assert_allclose(out["train"], g["train"], rtol=RTOL, atol=0)
+    np.testing.assert_allclose(out["test"], g["test"], rtol=RTOL, atol=0)
+    ref = g["elite_sem_sample"]
+    got = out["elite_train_semantics"][::int(g["sample_stride"][0])]
+    assert np.max(np.abs(got - ref)) <= RTOL * np.max(np.abs(ref))

@@ -89,7 +89,7 @@ def test_fitness_plan_gsm_survival_bit_exact():
 
 
 @pytest.mark.parametrize("name", ["tiny", "small", "plus", "g0", "accept", "c1", "wide", "m1", "k1",
-                                  "n1", "const", "funcs"])
+                                  "n1", "const", "funcs", "hugestep", "infstep"])
 def test_full_run_bit_exact(name):
     g = golden(f"run_{name}")
     cfg = R.Cfg(**ast.literal_eval(str(g["cfg"][0])))
@@ -113,3 +113,21 @@ def test_split_restatement_matches_reference():
         frac, seed = g[f"args_{n}"]
         tr, te = R.split_rows(n, float(frac), int(seed))
         assert np.array_equal(tr, g[f"tr_{n}"]) and np.array_equal(te, g[f"te_{n}"]), n
+
+
+@pytest.mark.parametrize("name", ["mid", "long"])
+def test_big_run_restatement_matches_reference(name):
+    """Headline-shape goldens (make_golden.py BIG_RUNS, data regenerated from
+    make_benchmark_dataset seeds): the restated loop equals the reference's
+    traces, elite records, plans and (sampled) elite semantics bit for bit."""
+    g = golden(f"big_{name}")
+    ntr, l, s1, nte, s2 = (int(x) for x in g["data"])
+    Xtr, ytr = R.benchmark_dataset(ntr, l, s1)
+    Xte, yte = R.benchmark_dataset(nte, l, s2)
+    out = R.run(R.Cfg(**ast.literal_eval(str(g["cfg"][0]))), Xtr, ytr, Xte, yte)
+    assert np.array_equal(out["train"], g["train"]) and np.array_equal(out["test"], g["test"])
+    assert [e[2] for e in out["elite"]] == g["slot"].tolist()
+    assert [e[1] for e in out["elite"]] == g["idx"].tolist()
+    assert np.array_equal(out["u"], g["u"]) and np.array_equal(out["v"], g["v"])
+    assert np.array_equal(out["ms"], g["ms"])
+    assert np.array_equal(out["elite_train_semantics"][::int(g["sample_stride"][0])], g["elite_sem_sample"])
