@@ -12,8 +12,9 @@
  *     from gsgp_last_error().  Python maps 1 -> ConfigError, others -> GsgpError.
  *   - All pointers are HOST pointers owned by the caller and pre-sized; the
  *     library owns all device memory.  Matrices are row-major, C-contiguous.
- *   - Not re-entrant: one call at a time per process.  Multi-GPU runs use one
- *     process per GPU (gsgp_comm_init) and shard the fitness cases.
+ *   - Not re-entrant: one call at a time per process.  Multi-GPU runs shard
+ *     the fitness cases either across processes (one per GPU, gsgp_comm_init)
+ *     or across the devices of one process (gsgp_init).
  *   - There is no CPU fallback: without a CUDA device every compute entry
  *     point fails with GSGP_ERR_CUDA.
  */
@@ -90,7 +91,24 @@ const char* gsgp_last_error(void);
 
 /* device count, SM count and name of the current device */
 int gsgp_device_info(int* device_count, int* sm_count, char* name, int name_len);
+/* one device per process from now on (clears a gsgp_init device set) */
 int gsgp_set_device(int device);
+
+/* Single-process multi-GPU (replaces the reference's worker pool behind
+ * run_evolution: gsgp/evolution.py:115, gsgp/backend.py:94-130 — one call
+ * uses every listed device).  After gsgp_init(n, ids) with n > 1, each
+ * gsgp_run drives the n devices from one host thread per device: the cases
+ * are sharded by device exactly as across processes, and the per-generation
+ * canonical-SSE collectives run over an NCCL communicator created with
+ * ncclCommInitAll.  Results are bit-identical to a one-device run.  A list
+ * that names a device twice (or GSGP_THREAD_EXCHANGE=1) uses a host thread
+ * exchange instead of NCCL (tests on one GPU).  n = 1 selects that device.
+ * Cannot be combined with gsgp_comm_init* (one process per GPU). */
+int gsgp_init(int n_dev, const int* dev_ids);
+/* destroy the device set's communicators; gsgp_run is single-device again */
+int gsgp_finalize(void);
+/* devices the next gsgp_run drives (0 = the current device, no set) */
+int gsgp_device_count_in_use(void);
 /* Return the engine's cached device memory (a run parks its device blocks
    for the next run instead of freeing them) and its pinned upload staging
    to the driver.  No reference

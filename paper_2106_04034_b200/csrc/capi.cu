@@ -23,6 +23,11 @@ void comm_init(int, int, const unsigned char*);
 void comm_destroy();
 void comm_init_host(int world, int rank, void (*fn)(void*, int64_t, int32_t));
 void trim_device_memory();
+void devices_init(int, const int*);
+void devices_finalize();
+int devices_count();
+void run_job(const gsgp_config*, const double*, const double*, int64_t, const double*, const double*, int64_t,
+             int32_t, gsgp_outputs*);
 void shard_range(int64_t, int64_t, int64_t, int64_t*, int64_t*);
 
 namespace {
@@ -123,6 +128,7 @@ int gsgp_device_info(int* device_count, int* sm_count, char* name, int name_len)
 int gsgp_set_device(int device) {
   return guarded([&] {
     require_device();
+    devices_finalize();            // back to one device per process
     GSGP_CUDA(cudaSetDevice(device));
   });
 }
@@ -463,9 +469,22 @@ int gsgp_run(const gsgp_config* cfg, const double* Xtr, const double* ytr, int64
              const double* yte, int64_t nte, int32_t n_features, gsgp_outputs* out) {
   return guarded([&] {
     require_device();
-    run_engine(cfg, Xtr, ytr, ntr, Xte, yte, nte, n_features, out);
+    run_job(cfg, Xtr, ytr, ntr, Xte, yte, nte, n_features, out);
   });
 }
+
+int gsgp_init(int n_dev, const int* dev_ids) {
+  return guarded([&] {
+    require_device();
+    devices_init(n_dev, dev_ids);
+  });
+}
+
+int gsgp_finalize(void) {
+  return guarded([&] { devices_finalize(); });
+}
+
+int gsgp_device_count_in_use(void) { return devices_count(); }
 
 int gsgp_comm_unique_id(unsigned char id[128]) {
   return guarded([&] { comm_unique_id(id); });

@@ -15,8 +15,10 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <condition_variable>
 #include <memory>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "gsgp_b200.h"
@@ -35,22 +37,42 @@ namespace gsgp {
 struct CachedBlock {
   void* p;
   size_t bytes;
+  int dev;          // blocks are only reused on the device that owns them
 };
 std::mutex g_cache_mu;
 std::vector<CachedBlock> g_cache;
 
-void cache_trim() {
+int current_device() {
+  int d = 0;
+  GSGP_CUDA(cudaGetDevice(&d));
+  return d;
+}
+
+// free the cached blocks of `dev` (-1: of every device)
+void cache_trim(int dev = -1) {
   std::lock_guard<std::mutex> lk(g_cache_mu);
-  for (auto& b : g_cache) cudaFree(b.p);
-  g_cache.clear();
+  int cur = 0;
+  cudaGetDevice(&cur);
+  std::vector<CachedBlock> keep;
+  for (auto& b : g_cache) {
+    if (dev >= 0 && b.dev != dev) {
+      keep.push_back(b);
+      continue;
+    }
+    cudaSetDevice(b.dev);
+    cudaFree(b.p);
+  }
+  cudaSetDevice(cur);
+  g_cache.swap(keep);
 }
 
 void* cache_alloc(size_t bytes, size_t* got) {
+  const int dev = current_device();
   {
     std::lock_guard<std::mutex> lk(g_cache_mu);
     int best = -1;
     for (int i = 0; i < (int)g_cache.size(); ++i)     // smallest block within 1.25x
-      if (g_cache[i].bytes >= bytes && g_cache[i].bytes <= bytes + bytes / 4 &&
+      if (g_cache[i].dev == dev && g_cache[i].bytes >= bytes && g_cache[i].bytes <= bytes + bytes / 4 &&
           (best < 0 || g_cache[i].bytes < g_cache[best].bytes))
         best = i;
     if (best >= 0) {
@@ -64,13 +86,14 @@ void* cache_alloc(size_t bytes, size_t* got) {
   cudaError_t e = cudaMalloc(&p, bytes);
   if (e == cudaErrorMemoryAllocation) {
     cudaGetLastError();
-    cache_trim();
+    cache_trim(dev);
     e = cudaMalloc(&p, bytes);
   }
   if (e != cudaSuccess) {
     cudaGetLastError();
     throw Error{e == cudaErrorMemoryAllocation ? ERR_OOM : ERR_CUDA,
-                "cudaMalloc(" + std::to_string(bytes) + " bytes): " + cudaGetErrorString(e)};
+                "cudaMalloc(" + std::to_string(bytes) + " bytes) on device " + std::to_string(dev) + ": " +
+                    cudaGetErrorString(e)};
   }
   *got = bytes;
   return p;
@@ -90,8 +113,10 @@ struct DevBuf {
     if (!p) return;
     // the block is parked for reuse by any stream: drain its stream first
     if (cudaStreamSynchronize(s) == cudaSuccess) {
+      int dev = 0;
+      cudaGetDevice(&dev);
       std::lock_guard<std::mutex> lk(g_cache_mu);
-      g_cache.push_back({p, bytes});
+      g_cache.push_back({p, bytes, dev});
     } else {
       cudaGetLastError();
       cudaFree(p);
@@ -125,8 +150,10 @@ struct NcclApi {
   void* h = nullptr;
   decltype(&ncclGetUniqueId) getUniqueId = nullptr;
   decltype(&ncclCommInitRank) commInitRank = nullptr;
+  decltype(&ncclCommInitAll) commInitAll = nullptr;
   decltype(&ncclAllReduce) allReduce = nullptr;
   decltype(&ncclCommDestroy) commDestroy = nullptr;
+  decltype(&ncclCommAbort) commAbort = nullptr;
   decltype(&ncclGetErrorString) errStr = nullptr;
 
   void load() {
@@ -137,10 +164,12 @@ struct NcclApi {
     if (!h) throw Error{ERR_NCCL, std::string("cannot load libnccl.so.2: ") + dlerror()};
     getUniqueId = (decltype(getUniqueId))dlsym(h, "ncclGetUniqueId");
     commInitRank = (decltype(commInitRank))dlsym(h, "ncclCommInitRank");
+    commInitAll = (decltype(commInitAll))dlsym(h, "ncclCommInitAll");
     allReduce = (decltype(allReduce))dlsym(h, "ncclAllReduce");
     commDestroy = (decltype(commDestroy))dlsym(h, "ncclCommDestroy");
+    commAbort = (decltype(commAbort))dlsym(h, "ncclCommAbort");
     errStr = (decltype(errStr))dlsym(h, "ncclGetErrorString");
-    if (!getUniqueId || !commInitRank || !allReduce || !commDestroy || !errStr)
+    if (!getUniqueId || !commInitRank || !commInitAll || !allReduce || !commDestroy || !commAbort || !errStr)
       throw Error{ERR_NCCL, "libnccl.so.2 lacks required symbols"};
   }
   void check(ncclResult_t r, const char* what) {
@@ -153,6 +182,15 @@ NcclApi& nccl() {
   return api;
 }
 
+// GSGP_FORCE_COLLECTIVES=1 (tests): a one-rank job still creates its NCCL
+// communicator and runs every collective through it, so the NCCL transport
+// (dlopen, allreduce, graph capture of the NCCL kernels) executes on a
+// one-GPU box; results must equal the collective-free path bit for bit.
+bool force_collectives() {
+  const char* e = getenv("GSGP_FORCE_COLLECTIVES");
+  return e && e[0] == '1';
+}
+
 // Host exchange (tests): the same collectives through a host callback that
 // reduces a host buffer over the ranks (e.g. torch.distributed over gloo), so
 // the multi-rank engine path runs with several processes on one GPU.  The
@@ -161,15 +199,57 @@ NcclApi& nccl() {
 enum HostRed : int32_t { kRedF64Sum = 0, kRedI32Sum = 1, kRedU64Sum = 2, kRedI32Max = 3 };
 typedef void (*HostAllreduce)(void* buf, int64_t count, int32_t dtype);
 
+// Thread exchange: the device threads of ONE process (gsgp_init with a
+// device list naming a GPU twice, or GSGP_THREAD_EXCHANGE=1) reduce through
+// host memory with a barrier, every thread summing the ranks' buffers in
+// rank order.  Lets the single-process multi-device driver run on one GPU.
+struct ThreadXchg {
+  int n = 1;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  int64_t phase = 0;
+  bool aborted = false;
+  std::vector<const unsigned char*> bufs;
+
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const int64_t ph = phase;
+    if (aborted) throw Error{ERR_CUDA, "another device thread of this run failed"};
+    if (++arrived == n) {
+      arrived = 0;
+      ++phase;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return phase != ph || aborted; });
+      if (aborted) throw Error{ERR_CUDA, "another device thread of this run failed"};
+    }
+  }
+  void abort() {
+    std::lock_guard<std::mutex> lk(mu);
+    aborted = true;
+    cv.notify_all();
+  }
+};
+
 struct CommState {
   ncclComm_t comm = nullptr;
   HostAllreduce host = nullptr;
+  ThreadXchg* tx = nullptr;
   int world = 1, rank = 0;
+  bool owns_comm = true;   // false: the comm belongs to the device set (gsgp_init)
 };
+// the process communicator (one process per GPU), or — inside a device
+// thread of a single-process multi-device run — that thread's own state
+thread_local CommState* t_comm = nullptr;
 CommState& comm_state() {
   static CommState c;
-  return c;
+  return t_comm ? *t_comm : c;
 }
+
+// collectives run when there is more than one rank or a communicator/exchange
+// exists (forced one-rank collectives)
+bool collective(const CommState& c) { return c.world > 1 || c.comm || c.tx; }
 
 void comm_unique_id(unsigned char* id) {
   nccl().load();
@@ -178,16 +258,24 @@ void comm_unique_id(unsigned char* id) {
   std::memcpy(id, u.internal, NCCL_UNIQUE_ID_BYTES);
 }
 
+void comm_reset(CommState& c) {
+  if (c.comm && c.owns_comm) nccl().commDestroy(c.comm);
+  c.comm = nullptr;
+  c.host = nullptr;
+  c.tx = nullptr;
+  c.world = 1;
+  c.rank = 0;
+  c.owns_comm = true;
+}
+
 void comm_init(int world, int rank, const unsigned char* id) {
   GSGP_REQUIRE(world >= 1 && rank >= 0 && rank < world, "bad world/rank");
+  GSGP_REQUIRE(t_comm == nullptr, "comm_init inside a device thread");
   CommState& c = comm_state();
-  if (c.comm) {
-    nccl().commDestroy(c.comm);
-    c.comm = nullptr;
-  }
+  comm_reset(c);
   c.world = world;
   c.rank = rank;
-  if (world == 1) return;
+  if (world == 1 && !force_collectives()) return;
   nccl().load();
   ncclUniqueId u;
   std::memcpy(u.internal, id, NCCL_UNIQUE_ID_BYTES);
@@ -197,26 +285,51 @@ void comm_init(int world, int rank, const unsigned char* id) {
 void comm_init_host(int world, int rank, HostAllreduce fn) {
   GSGP_REQUIRE(world >= 1 && rank >= 0 && rank < world && fn, "bad world/rank/callback");
   CommState& c = comm_state();
-  if (c.comm) {
-    nccl().commDestroy(c.comm);
-    c.comm = nullptr;
-  }
+  comm_reset(c);
   c.world = world;
   c.rank = rank;
   c.host = fn;
 }
 
-// in-place reduction over the ranks of a device buffer on stream s (NCCL or host)
+template <typename T, typename Op>
+void reduce_ranks(const std::vector<const unsigned char*>& bufs, int64_t count, unsigned char* dst, Op op) {
+  T* d = reinterpret_cast<T*>(dst);
+  for (int64_t e = 0; e < count; ++e) {
+    T a = reinterpret_cast<const T*>(bufs[0])[e];
+    for (size_t r = 1; r < bufs.size(); ++r) a = op(a, reinterpret_cast<const T*>(bufs[r])[e]);
+    d[e] = a;
+  }
+}
+
+// in-place reduction over the ranks of a device buffer on stream s (NCCL,
+// host callback or thread exchange)
 void allreduce(void* dev, int64_t count, HostRed kind, cudaStream_t s, const char* what) {
   CommState& c = comm_state();
-  if (c.world <= 1) return;
+  if (!collective(c)) return;
   const bool i32 = kind == kRedI32Sum || kind == kRedI32Max;
-  if (c.host) {
-    const size_t esz = i32 ? 4 : 8;
+  const size_t esz = i32 ? 4 : 8;
+  if (c.host || c.tx) {
     std::vector<unsigned char> h(count * esz);
     GSGP_CUDA(cudaMemcpyAsync(h.data(), dev, count * esz, cudaMemcpyDeviceToHost, s));
     GSGP_CUDA(cudaStreamSynchronize(s));
-    c.host(h.data(), count, (int32_t)kind);
+    if (c.host) {
+      c.host(h.data(), count, (int32_t)kind);
+    } else {
+      ThreadXchg& x = *c.tx;
+      x.bufs[c.rank] = h.data();
+      x.barrier();                                    // every rank's buffer is published
+      std::vector<unsigned char> acc(count * esz);
+      switch (kind) {
+        case kRedF64Sum: reduce_ranks<double>(x.bufs, count, acc.data(), [](double a, double b) { return a + b; }); break;
+        case kRedI32Sum: reduce_ranks<int32_t>(x.bufs, count, acc.data(), [](int32_t a, int32_t b) { return a + b; }); break;
+        case kRedU64Sum:
+          reduce_ranks<uint64_t>(x.bufs, count, acc.data(), [](uint64_t a, uint64_t b) { return a + b; });
+          break;
+        default: reduce_ranks<int32_t>(x.bufs, count, acc.data(), [](int32_t a, int32_t b) { return a > b ? a : b; });
+      }
+      x.barrier();                                    // every rank has read every buffer
+      h.swap(acc);
+    }
     GSGP_CUDA(cudaMemcpyAsync(dev, h.data(), count * esz, cudaMemcpyHostToDevice, s));
     GSGP_CUDA(cudaStreamSynchronize(s));
     return;
@@ -227,12 +340,8 @@ void allreduce(void* dev, int64_t count, HostRed kind, cudaStream_t s, const cha
 }
 
 void comm_destroy() {
-  CommState& c = comm_state();
-  if (c.comm) nccl().commDestroy(c.comm);
-  c.comm = nullptr;
-  c.host = nullptr;
-  c.world = 1;
-  c.rank = 0;
+  GSGP_REQUIRE(t_comm == nullptr, "comm_destroy inside a device thread");
+  comm_reset(comm_state());
 }
 
 // Contiguous case slices whose boundaries are multiples of kCaseAlign (the
@@ -280,16 +389,20 @@ inline unsigned nblk(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t
 // lifetime (grown on demand): page-locking a fresh buffer per run would cost
 // more than the copy it enables
 constexpr size_t kUploadChunkBytes = 48u << 20;
+constexpr int kMaxDevices = 64;
 struct PinnedStage {
   void* p = nullptr;
   size_t bytes = 0;
 };
-PinnedStage& pinned_stage_ref() {
-  static PinnedStage s;
-  return s;
+// one staging buffer per device: device threads of a multi-device run
+// upload concurrently
+PinnedStage& pinned_stage_ref(int dev) {
+  static PinnedStage s[kMaxDevices];
+  GSGP_REQUIRE(dev >= 0 && dev < kMaxDevices, "device ordinal out of range");
+  return s[dev];
 }
 PinnedStage& pinned_stage(size_t bytes) {
-  PinnedStage& s = pinned_stage_ref();
+  PinnedStage& s = pinned_stage_ref(current_device());
   // allocate the full double buffer on first use (page-locking ~100 MB costs
   // ~50 ms; growing it run by run would charge that to later runs)
   if (bytes < 2 * kUploadChunkBytes + (64u << 10)) bytes = 2 * kUploadChunkBytes + (64u << 10);
@@ -305,10 +418,12 @@ PinnedStage& pinned_stage(size_t bytes) {
 
 void trim_device_memory() {
   cache_trim();
-  PinnedStage& ps = pinned_stage_ref();
-  if (ps.p) cudaFreeHost(ps.p);
-  ps.p = nullptr;
-  ps.bytes = 0;
+  for (int d = 0; d < kMaxDevices; ++d) {
+    PinnedStage& ps = pinned_stage_ref(d);
+    if (ps.p) cudaFreeHost(ps.p);
+    ps.p = nullptr;
+    ps.bytes = 0;
+  }
 }
 
 struct Shard {
@@ -352,6 +467,7 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   GSGP_REQUIRE(G <= 16, "at most 16 virtual shards");
   CommState& cs = comm_state();
   const int W = cs.world;
+  const bool coll = collective(cs);   // exchange the per-rank sums (W > 1, or forced one-rank collectives)
   const int64_t nsh_total = (int64_t)W * G;
 
   cudaStream_t st, up;   // compute stream, host->device upload stream
@@ -643,7 +759,7 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
       if (interp_parts) launch_canon_exp(p->ipart.as<double>(), m, p->itiles, cexp.as<int32_t>(), s);
       else launch_canon_exp(p->part.as<double>(), m, p->ntiles, cexp.as<int32_t>(), s);
     }
-    if (W > 1) allreduce(cexp.p, m * 2, kRedI32Max, s, "ncclAllReduce(sse anchors)");
+    if (coll) allreduce(cexp.p, m * 2, kRedI32Max, s, "ncclAllReduce(sse anchors)");
     for (auto& p : sh) {
       if (p->pitch == 0) continue;
       if (interp_parts)
@@ -653,14 +769,19 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
         launch_canon_digits(p->part.as<double>(), m, p->ntiles, cexp.as<int32_t>(),
                             cdig.as<unsigned long long>(), s);
     }
-    if (W > 1) allreduce(cdig.p, m * 2 * kLimbs, kRedU64Sum, s, "ncclAllReduce(sse digits)");
+    if (coll) allreduce(cdig.p, m * 2 * kLimbs, kRedU64Sum, s, "ncclAllReduce(sse digits)");
     launch_canon_finish(cexp.as<int32_t>(), cdig.as<unsigned long long>(), m, dst, s);
   };
+  // GSGP_TEST_FAIL_RANK=i (tests): rank i of a multi-rank run fails here,
+  // while the other ranks wait in the first exchange, to check that a failed
+  // device thread aborts its peers instead of leaving them blocked
+  if (const char* f = getenv("GSGP_TEST_FAIL_RANK"))
+    if (coll && atoi(f) == cs.rank) throw Error{ERR_CUDA, "injected failure (GSGP_TEST_FAIL_RANK)"};
   canon_sse(false, sse_vec, st);
   canon_sse(true, sse64_vec, st);
   GSGP_CUDA(cudaStreamSynchronize(st));
   for (auto& p : sh) p->ipart.release();
-  if (W > 1) {
+  if (coll) {
     DevBuf bits;
     bits.alloc(m * 2 * 4);
     k_wide_split<<<nblk(m), 256, 0, st>>>(wide.as<int32_t>(), m, bits.as<int32_t>());
@@ -699,7 +820,7 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   DevBuf done;
   done.alloc(16);
   GSGP_CUDA(cudaMemsetAsync(done.p, 0, 16, st));
-  const bool fused_tail = (G == 1 && W == 1);
+  const bool fused_tail = (G == 1 && !coll);
   // fused tail: the GSM launch accumulates the canonical-sum anchors, the
   // reduce reads the partials once and re-arms the anchors (kExpZero)
   DevBuf gemax;
@@ -765,7 +886,7 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   if (g > 0) {
     cudaGraphExec_t exec = nullptr;
     cudaGraph_t graph = nullptr;
-    if (!timed && cfg->use_graph && !(W > 1 && cs.host)) {
+    if (!timed && cfg->use_graph && !cs.host && !cs.tx) {
       GSGP_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
       enqueue_generation(st, nullptr, nullptr);
       GSGP_CUDA(cudaStreamEndCapture(st, &graph));
@@ -854,5 +975,167 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   out->stage_ms[18] = ins_pop;    // instructions (not ms): population programs
   out->stage_ms[19] = ins_pool;   // instructions: random-tree programs
 }
+
+// ------------------------------------------------ single-process multi-GPU
+// gsgp_init(n_dev, dev_ids): one gsgp_run drives every listed
+// device from this process — one host thread per device, each running the
+// rank-sliced engine above as rank i of n with its own stream, and the
+// per-generation collectives over an NCCL communicator created with
+// ncclCommInitAll (the reference's run_evolution likewise uses every worker
+// of the host: gsgp/evolution.py:115, gsgp/backend.py:94-130).  A device list
+// that names a GPU twice (or GSGP_THREAD_EXCHANGE=1) runs the same threads
+// with the host thread exchange instead of NCCL, so the driver is testable on
+// one GPU.  Results equal the one-device run bit for bit (canonical SSE).
+struct DeviceSet {
+  std::vector<int> devs;
+  std::vector<ncclComm_t> comms;   // empty: thread exchange (or a single device)
+  bool thread_xchg = false;
+};
+std::mutex g_devset_mu;
+DeviceSet& device_set() {
+  static DeviceSet d;
+  return d;
+}
+
+void devices_release(DeviceSet& d) {
+  for (auto c : d.comms)
+    if (c) nccl().commDestroy(c);
+  d.comms.clear();
+  d.devs.clear();
+  d.thread_xchg = false;
+}
+
+void devices_init(int n, const int* ids) {
+  GSGP_REQUIRE(n >= 1 && n <= kMaxDevices && ids, "gsgp_init needs 1..64 device ids");
+  GSGP_REQUIRE(comm_state().world == 1 && !comm_state().comm && !comm_state().host,
+               "gsgp_init cannot be combined with a multi-process communicator (gsgp_comm_init*)");
+  int count = 0;
+  GSGP_CUDA(cudaGetDeviceCount(&count));
+  std::vector<int> devs(ids, ids + n);
+  bool dup = false;
+  for (int i = 0; i < n; ++i) {
+    GSGP_REQUIRE(devs[i] >= 0 && devs[i] < count,
+                 "device id " + std::to_string(devs[i]) + " out of range (" + std::to_string(count) + " devices)");
+    for (int j = 0; j < i; ++j) dup |= devs[j] == devs[i];
+  }
+  std::lock_guard<std::mutex> lk(g_devset_mu);
+  DeviceSet& d = device_set();
+  devices_release(d);
+  d.devs = devs;
+  const char* tx = getenv("GSGP_THREAD_EXCHANGE");
+  d.thread_xchg = n > 1 && (dup || (tx && tx[0] == '1'));
+  if ((n > 1 && !d.thread_xchg) || (n == 1 && force_collectives())) {
+    nccl().load();
+    d.comms.assign(n, nullptr);
+    nccl().check(nccl().commInitAll(d.comms.data(), n, d.devs.data()), "ncclCommInitAll");
+  }
+  GSGP_CUDA(cudaSetDevice(devs[0]));
+}
+
+void devices_finalize() {
+  std::lock_guard<std::mutex> lk(g_devset_mu);
+  devices_release(device_set());
+}
+
+int devices_count() { return (int)device_set().devs.size(); }
+
+void run_job(const gsgp_config* cfg, const double* Xtr, const double* ytr, int64_t ntr, const double* Xte,
+             const double* yte, int64_t nte, int32_t l, gsgp_outputs* out) {
+  std::unique_lock<std::mutex> lk(g_devset_mu);
+  DeviceSet& d = device_set();
+  const int n = (int)d.devs.size();
+  if (n <= 1 && d.comms.empty()) {              // one device: this thread runs the engine
+    if (n == 1) GSGP_CUDA(cudaSetDevice(d.devs[0]));
+    lk.unlock();
+    run_engine(cfg, Xtr, ytr, ntr, Xte, yte, nte, l, out);
+    return;
+  }
+  GSGP_REQUIRE(cfg && out, "null config/outputs");
+  const int64_t g = cfg->generations < 0 ? 0 : cfg->generations;
+  // rank 0 writes the caller's outputs; the other ranks compute the same
+  // traces and lineage into scratch (checked equal below) and their case
+  // slice of the elite train semantics into the caller's buffer
+  struct Scratch {
+    std::vector<double> tr, te, fit;
+    std::vector<int8_t> src;
+    std::vector<int64_t> idx, slot;
+  };
+  std::vector<gsgp_outputs> outs(n, *out);
+  std::vector<Scratch> scr(n);
+  for (int i = 1; i < n; ++i) {
+    Scratch& q = scr[i];
+    q.tr.resize(g + 1); q.te.resize(g + 1); q.fit.resize(g + 1);
+    q.src.resize(g + 1); q.idx.resize(g + 1); q.slot.resize(g + 1);
+    gsgp_outputs& o = outs[i];
+    o.train_trace = q.tr.data(); o.test_trace = q.te.data(); o.elite_fit = q.fit.data();
+    o.elite_src = q.src.data(); o.elite_idx = q.idx.data(); o.elite_slot = q.slot.data();
+    o.plan_u = o.plan_v = nullptr;
+    o.plan_ms = nullptr;
+    o.gsm_ms = nullptr;
+  }
+  ThreadXchg tx;
+  tx.n = n;
+  tx.bufs.assign(n, nullptr);
+  std::vector<Error> errs(n, Error{0, ""});
+  const std::vector<ncclComm_t> comms = d.comms;
+  std::mutex abort_mu;
+  bool aborted = false;
+  auto abort_all = [&] {       // a failed rank must not leave the others blocked in a collective
+    std::lock_guard<std::mutex> g(abort_mu);
+    if (aborted) return;
+    aborted = true;
+    tx.abort();
+    for (auto c : comms)
+      if (c) nccl().commAbort(c);
+  };
+  std::vector<std::thread> th;
+  for (int i = 0; i < n; ++i)
+    th.emplace_back([&, i] {
+      CommState cs;
+      cs.world = n;
+      cs.rank = i;
+      cs.owns_comm = false;
+      if (comms.empty()) cs.tx = &tx;
+      else cs.comm = comms[i];
+      t_comm = &cs;
+      try {
+        GSGP_CUDA(cudaSetDevice(d.devs[i]));
+        run_engine(cfg, Xtr, ytr, ntr, Xte, yte, nte, l, &outs[i]);
+      } catch (const Error& e) {
+        errs[i] = e;
+        abort_all();
+      } catch (const std::exception& e) {
+        errs[i] = Error{ERR_CUDA, e.what()};
+        abort_all();
+      }
+      t_comm = nullptr;
+    });
+  for (auto& t : th) t.join();
+  if (aborted) {                           // the communicators are gone: gsgp_init again
+    d.comms.clear();
+    d.devs.clear();
+  }
+  for (int i = 0; i < n; ++i)              // the first failure that is not the abort echo
+    if (errs[i].code && errs[i].msg.find("another device thread") == std::string::npos)
+      throw Error{errs[i].code, "device " + std::to_string(i) + ": " + errs[i].msg};
+  for (int i = 0; i < n; ++i)
+    if (errs[i].code) throw Error{errs[i].code, "device " + std::to_string(i) + ": " + errs[i].msg};
+  // every rank took the same decisions from the same exchanged sums
+  for (int i = 1; i < n; ++i)
+    for (int64_t t = 0; t <= g; ++t)
+      if (outs[i].elite_slot[t] != out->elite_slot[t] || outs[i].elite_idx[t] != out->elite_idx[t] ||
+          std::memcmp(&outs[i].train_trace[t], &out->train_trace[t], 8) != 0)
+        throw Error{ERR_CUDA, "device ranks diverged at generation " + std::to_string(t)};
+  *out = outs[0];
+  out->shard_train_lo = outs[0].shard_train_lo;
+  out->shard_train_hi = outs[n - 1].shard_train_hi;
+  // device time of the job = the slowest rank; launches = all ranks' kernels
+  for (int q : {1, 2, 4, 8, 12, 13, 14, 15})
+    for (int i = 1; i < n; ++i) out->stage_ms[q] = std::max(out->stage_ms[q], outs[i].stage_ms[q]);
+  out->stage_ms[3] = g > 0 ? out->stage_ms[2] / (double)g : 0.0;
+  for (int q : {6, 7, 10, 11})
+    for (int i = 1; i < n; ++i) out->stage_ms[q] += outs[i].stage_ms[q];
+}
+
 
 }  // namespace gsgp

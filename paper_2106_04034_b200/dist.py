@@ -18,7 +18,7 @@ import ctypes as C
 
 import numpy as np
 
-from . import _lib
+from . import _lib, devices
 from ._lib import check
 
 
@@ -48,7 +48,9 @@ def init_from_torch(group=None) -> tuple[int, int]:
     payload = [bytes(uid)]
     td.broadcast_object_list(payload, src=0, group=group)
     buf = (C.c_ubyte * 128).from_buffer_copy(payload[0])
+    devices.activate(None)
     check(lib.gsgp_comm_init(world, rank, buf))
+    devices._process_comm = True
     return world, rank
 
 
@@ -80,12 +82,15 @@ def init_host_exchange(group=None) -> tuple[int, int]:
         arr[:] = t.numpy().view(npt) if npt is np.uint64 else t.numpy()
 
     _host_cb = HOST_ALLREDUCE(allreduce)
+    devices.activate(None)
     check(_lib.load().gsgp_comm_init_host(world, rank, C.cast(_host_cb, C.c_void_p)))
+    devices._process_comm = True
     return world, rank
 
 
 def destroy() -> None:
     check(_lib.load().gsgp_comm_destroy())
+    devices._process_comm = False
 
 
 def gather_elite_semantics(result, n_train: int, group=None) -> np.ndarray:

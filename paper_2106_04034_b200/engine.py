@@ -15,7 +15,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import _lib, ops
+from . import _lib, devices as _devices, ops
 from ._lib import check, ptr
 from .core import (
     ConfigError, Dataset, EliteRecord, LineageEntry, LineageError, LineageLog, MutationPlan,
@@ -70,7 +70,7 @@ class RunResult:
 
 def run_evolution(cfg: RunConfig, train: Dataset, test: Dataset, *, storage: str = "fp32",
                   use_graph: bool = True, time_kernels: bool = False,
-                  virtual_shards: int = 1, window_start: int = 0) -> RunResult:
+                  virtual_shards: int = 1, window_start: int = 0, devices="auto") -> RunResult:
     """gsgp/evolution.py:100-179 on the B200.
 
     storage: "fp32" (default; semantics stored in fp32, interpreter and SSE in
@@ -81,6 +81,11 @@ def run_evolution(cfg: RunConfig, train: Dataset, test: Dataset, *, storage: str
     time_kernels records CUDA events around every GSM launch (direct launches
     instead of the replayed graph); window_start opens a device-timed window
     over generations window_start+1..g (`device["window_ms"]`).
+    devices: the GPUs this one call drives (devices.py: "auto" = every
+    visible GPU the workload can use, one per 2 GiB of population semantics;
+    "all"; an int n; a list of ids; None = the current device).  Several
+    devices shard the cases by device inside this process (one host thread
+    and one NCCL rank per GPU) and give the same bits as one device.
     """
     if train.n_features != test.n_features:
         raise ConfigError(f"train has {train.n_features} features but test has {test.n_features}")
@@ -101,9 +106,14 @@ def run_evolution(cfg: RunConfig, train: Dataset, test: Dataset, *, storage: str
     )
     for name, arr in arrays.items():
         setattr(out, name, ptr(arr))
+    ids = _devices.resolve(devices, m, train.n_cases + test.n_cases)
+    _devices.activate(ids)
     t_call = t_call_start = time.perf_counter()
-    check(_lib.load().gsgp_run(C.byref(s), ptr(Xtr), ptr(ytr), train.n_cases, ptr(Xte), ptr(yte),
-                               test.n_cases, train.n_features, C.byref(out)))
+    rc = _lib.load().gsgp_run(C.byref(s), ptr(Xtr), ptr(ytr), train.n_cases, ptr(Xte), ptr(yte),
+                               test.n_cases, train.n_features, C.byref(out))
+    if rc and ids is not None and _lib.load().gsgp_device_count_in_use() != len(ids):
+        _devices.reset()          # a failed multi-device run dropped its communicators
+    check(rc)
     t_call = (time.perf_counter() - t_call) * 1e3
     a = arrays
     log = LineageLog(EliteRecord("initial", int(a["elite_idx"][0]), int(a["elite_slot"][0]),
@@ -128,6 +138,7 @@ def run_evolution(cfg: RunConfig, train: Dataset, test: Dataset, *, storage: str
                           "interpret_pool": st[14], "initial_sse": st[15], "compile": st[16],
                           "alloc": st[17]},
               "program_instructions": {"population": int(st[18]), "pool": int(st[19])},
+              "devices": list(ids) if ids is not None else None,
               "storage": "fp64" if out.storage_f64_used else "fp32",
               "storage_requested": storage,
               "interpreter": {"config": int(out.interp_info[0]), "max_spill_depth": int(out.interp_info[1]),

@@ -60,8 +60,15 @@ def select_local_device() -> None:
     """Bind this process to its GPU (LOCAL_RANK) before its first run
     (GSGP_SHARED_GPU=1: every rank on GPU 0, for tests on a one-GPU box)."""
     from . import _lib
+    from . import devices
     local = 0 if os.environ.get("GSGP_SHARED_GPU") == "1" else int(os.environ.get("LOCAL_RANK", "0"))
     _lib.check(_lib.load().gsgp_set_device(local))
+    devices.reset()
+
+
+def _device_run(cfg, train, test, **kw):
+    from .engine import run_evolution
+    return run_evolution(cfg, train, test, **kw)
 
 
 def run_many(cfg: RunConfig, train, test, *, group=None, gather: str = "results", run_fn=None,
@@ -78,12 +85,14 @@ def run_many(cfg: RunConfig, train, test, *, group=None, gather: str = "results"
     if gather not in ("results", "summary", "none"):
         raise ConfigError("gather must be 'results', 'summary' or 'none'")
     if run_fn is None:
-        from .engine import run_evolution as run_fn
+        run_fn = _device_run
     world, rank, td = _world(group)
     seeds = run_seeds(cfg)
     mine = assign_runs(cfg.runs, world, rank)
     out: list = [None] * cfg.runs
     failure = None
+    if world > 1 and run_fn is _device_run:
+        engine_kw.setdefault("devices", None)     # replicas: each rank keeps its own GPU
     for i in mine:
         try:
             res = run_fn(cfg.with_seed(seeds[i]), train, test, **engine_kw)
