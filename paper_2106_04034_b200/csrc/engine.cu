@@ -394,36 +394,52 @@ struct PinnedStage {
   void* p = nullptr;
   size_t bytes = 0;
 };
-// one staging buffer per device: device threads of a multi-device run
-// upload concurrently
-PinnedStage& pinned_stage_ref(int dev) {
-  static PinnedStage s[kMaxDevices];
-  GSGP_REQUIRE(dev >= 0 && dev < kMaxDevices, "device ordinal out of range");
-  return s[dev];
-}
-PinnedStage& pinned_stage(size_t bytes) {
-  PinnedStage& s = pinned_stage_ref(current_device());
-  // allocate the full double buffer on first use (page-locking ~100 MB costs
-  // ~50 ms; growing it run by run would charge that to later runs)
-  if (bytes < 2 * kUploadChunkBytes + (64u << 10)) bytes = 2 * kUploadChunkBytes + (64u << 10);
-  if (s.bytes < bytes) {
-    if (s.p) GSGP_CUDA(cudaFreeHost(s.p));
-    s.p = nullptr;
-    s.bytes = 0;
-    GSGP_CUDA(cudaHostAlloc(&s.p, bytes, cudaHostAllocDefault));
-    s.bytes = bytes;
+// Pinned staging buffers are pooled for the process lifetime: a run takes
+// one (the device threads of a multi-device run each take their own, even
+// when they share a GPU), uses it for every chunked upload, and returns it
+// at the end, so the next run neither page-locks nor frees ~100 MB again.
+std::mutex g_pin_mu;
+std::vector<PinnedStage> g_pin_free;
+
+struct PinnedLease {
+  PinnedStage st{};
+  PinnedLease() = default;
+  PinnedLease(const PinnedLease&) = delete;
+  PinnedLease& operator=(const PinnedLease&) = delete;
+  ~PinnedLease() {
+    if (!st.p) return;
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    g_pin_free.push_back(st);
   }
-  return s;
-}
+  // at least `bytes`; the first use takes the full double buffer (page-locking
+  // costs ~50 ms per 100 MB, which growing run by run would charge to later runs)
+  PinnedStage& get(size_t bytes) {
+    if (bytes < 2 * kUploadChunkBytes + (64u << 10)) bytes = 2 * kUploadChunkBytes + (64u << 10);
+    if (st.bytes >= bytes) return st;
+    {
+      std::lock_guard<std::mutex> lk(g_pin_mu);
+      if (st.p) g_pin_free.push_back(st);
+      st = PinnedStage{};
+      int best = -1;
+      for (int i = 0; i < (int)g_pin_free.size(); ++i)
+        if (g_pin_free[i].bytes >= bytes && (best < 0 || g_pin_free[i].bytes < g_pin_free[best].bytes)) best = i;
+      if (best >= 0) {
+        st = g_pin_free[best];
+        g_pin_free.erase(g_pin_free.begin() + best);
+        return st;
+      }
+    }
+    GSGP_CUDA(cudaHostAlloc(&st.p, bytes, cudaHostAllocPortable));
+    st.bytes = bytes;
+    return st;
+  }
+};
 
 void trim_device_memory() {
   cache_trim();
-  for (int d = 0; d < kMaxDevices; ++d) {
-    PinnedStage& ps = pinned_stage_ref(d);
-    if (ps.p) cudaFreeHost(ps.p);
-    ps.p = nullptr;
-    ps.bytes = 0;
-  }
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  for (auto& ps : g_pin_free) cudaFreeHost(ps.p);
+  g_pin_free.clear();
 }
 
 struct Shard {
@@ -565,6 +581,7 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   GSGP_CUDA(cudaMemcpyAsync(hlen.data(), plen.p, ng * 4, cudaMemcpyDeviceToHost, st));
   GSGP_CUDA(cudaStreamSynchronize(st));
 
+  PinnedLease pin_lease;   // this run's pinned upload staging
   // ---- per shard: upload the case slice, interpret population and pool
   double init_phase_ms[4] = {0, 0, 0, 0};   // upload, population, pool, initial SSE
   double alloc_ms = 0.0;                     // host clock: device allocations + clears
@@ -649,7 +666,7 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
     if (chunk < 3072) chunk = 3072;
     if (chunk > Nq) chunk = (Nq + itile - 1) / itile * itile;
     const int64_t nchunks = (Nq + chunk - 1) / chunk;
-    PinnedStage& pin = pinned_stage(2 * (size_t)chunk * row_bytes);
+    PinnedStage& pin = pin_lease.get(2 * (size_t)chunk * row_bytes);
     DevBuf Xr[2], XT[2];
     for (int b = 0; b < 2 && b < nchunks; ++b) {
       Xr[b].alloc(chunk * l * 8);
