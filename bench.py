@@ -10,15 +10,18 @@ generations are timed on the device with CUDA events (the engine records
 the window events on its stream).  Default workload: C3 = pop 1024, 8
 features, 10M train + 2.5M test cases, random-tree pool 1024, k=1024 — the
 configuration the metric is quoted on at 1/2/4/8 B200 (cases sharded by
-rank, strong scaling); it fits one GPU (~103 GB).
+GPU, strong scaling); it fits one GPU (~103 GB).  N > 1 GPUs: under
+torchrun one process per GPU; without it, --gpus N drives N GPUs from this
+process (gsgp_init: one host thread and one NCCL rank per device).
 
 Printed JSON line (rank 0): value = generations/s of the whole job; e2e =
 the same metric through the public `run_evolution` call from host numpy
 datasets (H2D, init, loop and D2H inside the timed region); roofline = the
 fused GSM+SSE kernel's algorithmic bytes (4*N*(2m+D_g+1) per
-generation) over its CUDA-event time; cpu_baseline = the reference loop
-(oracle port) on this host's cores.  `--impl reference` times that CPU
-reference path alone, in bounded per-step samples.
+generation) over its CUDA-event time; cpu_baseline = the reference's own
+generation body (baseline/_ref gsgp 0.1.0, all host cores) on a bounded case
+sample.  `--impl reference` times that CPU reference path alone, one
+generation per step.
 """
 
 from __future__ import annotations
@@ -148,40 +151,94 @@ def interp_line(res, c, world: int) -> dict:
             "bound": "issue/fp64 latency (see DESIGN.md §6)"}
 
 
-def cpu_leg(c, budget_s: float):
-    from oracle import cpu_bench
-    t = cpu_bench.time_loop(c["m"], c["r"], c["ntr"], c["nte"], budget_s=budget_s,
-                            max_cases=125_000, workers=os.cpu_count())
+def workload_config(c) -> dict:
+    """The `config` object of BOTH arms (identical by construction)."""
+    return {"workload": c["desc"], "m": c["m"], "r": c["r"], "k": c["k"], "features": c["l"],
+            "n_train": c["ntr"], "n_test": c["nte"],
+            "l2": ("inputs larger than L2 (population and pool semantics "
+                   f"{4 * c['m'] * (c['ntr'] + c['nte']) / 1e9:.1f} GB each)")
+            if c["ntr"] > 1_000_000 else "small config: L2-resident"}
+
+
+def ref_sample(c, max_cases=125_000):
+    """Case sample of the CPU reference legs: the whole workload when it has
+    at most `max_cases` cases, else max_cases in the workload's train:test
+    ratio (C3-C5 timed at 100k+25k and scaled linearly in N,
+    the reference's O(m*g*n/t))."""
     N = c["ntr"] + c["nte"]
-    sample = (f"reference generation body (oracle port of gsgp/evolution.py:146-158, numpy, "
-              f"{t['workers']} threads) on synthetic fp64 state m={c['m']} r={c['r']} with "
-              f"{t['sample_train']}+{t['sample_test']} cases, {t['gens_timed']} timed generations")
-    if t["case_fraction"] < 1.0:
-        sample += f", rate scaled linearly from {t['sample_train'] + t['sample_test']} to {N} cases"
-    return {"value": t["gen_per_s"], "unit": METRIC, "cores": t["workers"], "kind": "port",
-            "sample": sample, "cpu": cpu_bench.cpu_model(),
+    if N <= max_cases:
+        return c["ntr"], c["nte"], 1.0
+    s_tr = int(round(max_cases * c["ntr"] / N))
+    s_te = max_cases - s_tr
+    return s_tr, s_te, max_cases / N
+
+
+def cpu_leg(c, budget_s: float):
+    """cpu_baseline: the reference's own generation body (baseline/_ref,
+    oracle/ref_bench.py) on this host — all cores through its ThreadBackend
+    (the value) and its SequentialBackend — else the numpy port."""
+    from oracle import cpu_bench, ref_bench
+    s_tr, s_te, frac = ref_sample(c)
+    workers = os.cpu_count() or 1
+    gsgp, why = ref_bench.import_reference()
+    if gsgp is not None:
+        thr = ref_bench.ref_generations(c["m"], c["r"], s_tr, s_te, backend="threads",
+                                        budget_s=budget_s * 0.6, min_gens=3)
+        seq = ref_bench.ref_generations(c["m"], c["r"], s_tr, s_te, backend="sequential",
+                                        budget_s=budget_s * 0.3, min_gens=1, warmup=0)
+        sample = (f"reference gsgp 0.1.0 (baseline/_ref, unmodified) generation body "
+                  f"(gsgp/evolution.py:146-158: build_mutation_plan, _gsm_squashed x2, compute_fitness, "
+                  f"survive, rmse) with get_backend('threads', 0) = {thr['workers']} threads, "
+                  f"m={c['m']} r={c['r']} on {s_tr}+{s_te} cases (synthetic fp64 state), "
+                  f"{thr['gens_timed']} timed generations")
+        if frac < 1.0:
+            sample += f", rate scaled linearly from {s_tr + s_te} to {c['ntr'] + c['nte']} cases"
+        return {"value": frac / thr["sec_per_gen"], "unit": METRIC, "cores": thr["workers"],
+                "kind": "reference", "sample": sample, "cpu": cpu_bench.cpu_model(),
+                "sec_per_gen_sample": thr["sec_per_gen"],
+                "sequential": {"value": frac / seq["sec_per_gen"], "cores": 1,
+                               "sec_per_gen_sample": seq["sec_per_gen"], "gens_timed": seq["gens_timed"]}}
+    t = cpu_bench.time_loop(c["m"], c["r"], s_tr, s_te, budget_s=budget_s, workers=workers)
+    sample = (f"oracle port of gsgp/evolution.py:146-158 (numpy, {t['workers']} threads; {why}) on "
+              f"synthetic fp64 state m={c['m']} r={c['r']} with {s_tr}+{s_te} cases, "
+              f"{t['gens_timed']} timed generations")
+    if frac < 1.0:
+        sample += f", rate scaled linearly from {s_tr + s_te} to {c['ntr'] + c['nte']} cases"
+    return {"value": t["sec_per_gen_sample"] and frac / t["sec_per_gen_sample"], "unit": METRIC,
+            "cores": t["workers"], "kind": "port", "sample": sample, "cpu": cpu_bench.cpu_model(),
             "sec_per_gen_sample": t["sec_per_gen_sample"]}
 
 
 def run_ours(args):
     world, rank, local = dist_env()
+    if world > 1 and args.gpus != world:
+        raise SystemExit(f"--gpus {args.gpus} but torchrun started {world} ranks")
     td = None
     if world > 1:
         import torch.distributed as td
         td.init_process_group("gloo", rank=rank, world_size=world)
     import paper_2106_04034_b200 as G
-    from paper_2106_04034_b200 import _lib, dist
+    from paper_2106_04034_b200 import _lib, devices, dist
     lib = _lib.load()
     # GSGP_BENCH_HOST_EXCHANGE=1: harness check of the N>1 path with every
     # rank on GPU 0 and the collectives over host memory + gloo (no NCCL);
     # its numbers are not bench values
     host_xchg = world > 1 and os.environ.get("GSGP_BENCH_HOST_EXCHANGE") == "1"
     _lib.check(lib.gsgp_set_device(0 if host_xchg else local))
+    devices.reset()
     if world > 1:
         if host_xchg:
             dist.init_host_exchange()
         else:
             dist.init_from_torch()
+    # without torchrun, --gpus N > 1 drives N GPUs from this one process
+    # (gsgp_init: one host thread and one NCCL rank per device)
+    in_proc = args.gpus if world == 1 and args.gpus > 1 else None
+    if in_proc is not None and devices.visible_device_count() < in_proc:
+        raise SystemExit(f"--gpus {in_proc} but only {devices.visible_device_count()} GPUs are visible")
+    n_gpus = world * (in_proc or 1)
+    ranks = n_gpus
+    shard = rank if world > 1 else 0           # the shard whose kernel time the roofline uses
 
     def barrier():
         if td:
@@ -206,24 +263,24 @@ def run_ours(args):
     sampler = ClockSampler(local)
     sampler.start()
     barrier()
-    res = G.run_evolution(cfg, train, test, time_kernels=True, window_start=W)
+    res = G.run_evolution(cfg, train, test, time_kernels=True, window_start=W, devices=in_proc)
     barrier()
     clocks = sampler.summary()
-    win_ms = max_over_ranks(res.device["window_ms"])
+    win_ms = max_over_ranks(res.device["window_ms"])     # engine: max over its device threads
     value = K / (win_ms / 1e3)
 
-    lo, hi = res.device["shard_train_range"]
-    te_lo, te_hi = dist.shard_range(c["nte"], world, rank)
-    n_local = (hi - lo) + (te_hi - te_lo)     # cases this rank's kernel streams
+    lo, hi = dist.shard_range(c["ntr"], ranks, shard)
+    te_lo, te_hi = dist.shard_range(c["nte"], ranks, shard)
+    n_local = (hi - lo) + (te_hi - te_lo)     # cases this shard's kernel streams
     plans = [(e.plan.u, e.plan.v) for e in res.lineage.entries[W:]]
     bpg = bytes_per_generation(plans, n_local, c["m"])
-    gsm_ms = res.device["window_gsm_ms"]
-    launches = max(res.device["window_gsm_launches"], 1)
+    gsm_ms = res.device["window_gsm_ms"]      # shard 0 of this process (rank 0's device thread)
+    launches = max(res.device["window_gsm_launches"] // (in_proc or 1), 1)
     achieved = float(bpg.sum() / (gsm_ms / 1e3) / 1e9)
     peak, peak_kind = peaks()
     traffic = None
     tfile = ROOT / "profiles" / "gsm_traffic.json"
-    if tfile.exists():
+    if tfile.exists() and n_gpus == 1:
         try:
             traffic = json.loads(tfile.read_text()).get(args.config)
         except Exception:
@@ -236,7 +293,7 @@ def run_ours(args):
                            generations=K, seed=1)
         barrier()
         t0 = time.perf_counter()
-        res2 = G.run_evolution(cfg2, train, test)
+        res2 = G.run_evolution(cfg2, train, test, devices=in_proc)
         barrier()
         wall = max_over_ranks(time.perf_counter() - t0)
         h2d = (train.features.nbytes + train.target.nbytes + test.features.nbytes + test.target.nbytes)
@@ -253,19 +310,19 @@ def run_ours(args):
                "init_phases_ms": res2.device["init_ms"]}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and n_gpus == 1 and not args.no_cpu_baseline:
         cpu = cpu_leg(c, args.cpu_budget)
 
     # secondary single-GPU line on C2 (configs[1]) for context, same method
     secondary = None
-    if world == 1 and args.config == "c3" and not args.no_secondary:
+    if n_gpus == 1 and args.config == "c3" and not args.no_secondary:
         c2 = CONFIGS["c2"]
         tr2 = G.make_benchmark_dataset(c2["ntr"], c2["l"], seed=1)
         te2 = G.make_benchmark_dataset(c2["nte"], c2["l"], seed=2)
         K2 = 500
         r2 = G.run_evolution(G.RunConfig(population_size=c2["m"], random_trees=c2["r"],
                                          program_size=c2["k"], generations=W + K2, seed=1),
-                             tr2, te2, time_kernels=True, window_start=W)
+                             tr2, te2, time_kernels=True, window_start=W, devices=None)
         b2 = bytes_per_generation([(e.plan.u, e.plan.v) for e in r2.lineage.entries[W:]],
                                   c2["ntr"] + c2["nte"], c2["m"])
         a2 = float(b2.sum() / (r2.device["window_gsm_ms"] / 1e3) / 1e9)
@@ -276,28 +333,29 @@ def run_ours(args):
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": "generations/s", "n_gpus": world,
+            "metric": METRIC, "value": value, "unit": "generations/s", "n_gpus": n_gpus,
             "steps": K, "warmup": W, "ms_per_step": win_ms / K, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32 storage / f64 interp+SSE",
             "data": "synthetic (make_benchmark_dataset: U[-1,1) features, x0*x1+sum(x) target)",
-            "config": {"workload": c["desc"], "m": c["m"], "r": c["r"], "k": c["k"],
-                       "features": c["l"], "n_train": c["ntr"], "n_test": c["nte"],
-                       "parallelism": f"case-shard x{world}",
-                       "l2": "inputs larger than L2 (population and pool semantics "
-                             f"{4 * c['m'] * (c['ntr'] + c['nte']) / 1e9:.1f} GB each)"
-                       if c["ntr"] > 1_000_000 else "small config: L2-resident"},
+            "config": workload_config(c),
+            "impl": "ours",
+            "parallelism": (f"case-shard x{n_gpus}: " +
+                            ("one process per GPU (torchrun, NCCL)" if world > 1 else
+                             "one process, one host thread + NCCL rank per GPU (gsgp_init)"
+                             if in_proc else "single GPU")),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "k_gsm<float> (fused GSM+SSE, train+test)",
+                         "kernel": "k_gsm_tma<float> (fused GSM+SSE, train+test)",
                          "peak_kind": peak_kind,
                          "algorithmic_bytes_per_launch": float(bpg.mean()),
                          "avg_launch_ms": gsm_ms / launches,
-                         "kernel_share_of_step": gsm_ms / win_ms},
+                         "kernel_share_of_step": gsm_ms / win_ms,
+                         "shard": f"{shard} of {ranks} ({n_local} cases)"},
             "e2e": e2e,
             "cpu_baseline": cpu,
-            "gpu_launches": res.device["window_loop_launches"],
+            "gpu_launches": res.device["window_loop_launches"] * (world if world > 1 else 1),
             "clocks": clocks,
-            "interpreter": interp_line(res, c, world),
+            "interpreter": interp_line(res, c, ranks),
             "init_ms": {"create_population": res.timings.create_population_ms,
                         "compute_semantics": res.timings.compute_semantics_ms,
                         **res.device["init_ms"]},
@@ -310,47 +368,54 @@ def run_ours(args):
     if world > 1:
         dist.destroy()
         td.destroy_process_group()
+    else:
+        devices.activate(None)
 
 
 def run_reference(args):
-    """CPU reference path (oracle port: the reference is pure Python and has
-    no compiled form) on this host's cores; each step is one reference
-    generation over a bounded case sample, value scaled to the full config."""
+    """The reference's own CPU code (baseline/_ref gsgp 0.1.0, oracle/ref_bench.py)
+    on this host's cores: each step is one generation of the reference's
+    generation body with its ThreadBackend over every core, on the workload's
+    case sample (ref_sample), value scaled to the full config; the numpy port
+    stands in when baseline/_ref is missing."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    from oracle import cpu_bench
+    from oracle import cpu_bench, ref_bench
     c = CONFIGS[args.config]
     K, W = args.steps, args.warmup
     N = c["ntr"] + c["nte"]
+    s_tr, s_te, frac = ref_sample(c)
     workers = os.cpu_count() or 1
-    # probe the per-case cost, then size a step to ~min(0.5 s, 150 s / (K+W))
-    probe_cases = min(N, 20_000)
-    p = cpu_bench.time_loop(c["m"], c["r"], int(probe_cases * 0.8), probe_cases - int(probe_cases * 0.8),
-                            budget_s=0.0, workers=workers, min_gens=1, warmup=1)
-    step_s = min(0.5, 150.0 / max(K + W, 1))
-    n_s = min(N, cpu_bench.sample_cases_for(step_s, c["m"], (probe_cases, p["sec_per_gen_sample"])))
-    s_tr = max(1, int(round(n_s * c["ntr"] / N)))
-    s_te = max(1, n_s - s_tr)
-    st = cpu_bench.LoopState(c["m"], c["r"], s_tr, s_te)
-    for w in range(W):
-        st.generation(w + 1, workers=workers)
-    t0 = time.perf_counter()
-    for k in range(K):
-        st.generation(W + k + 1, workers=workers)
-    dt = time.perf_counter() - t0
-    frac = (s_tr + s_te) / N
+    gsgp, why = ref_bench.import_reference()
+    if gsgp is not None:
+        kind = "reference"
+        r = ref_bench.ref_generations(c["m"], c["r"], s_tr, s_te, backend="threads", warmup=W, gens=K)
+        dt = sum(r["times"])
+        workers = r["workers"]
+        sample = (f"each step = one generation of the reference gsgp 0.1.0 (baseline/_ref, unmodified: "
+                  f"gsgp/evolution.py:146-158 with get_backend('threads', 0), {workers} threads) on "
+                  f"{s_tr}+{s_te} cases of synthetic fp64 state")
+    else:
+        kind = "port"
+        st = cpu_bench.LoopState(c["m"], c["r"], s_tr, s_te)
+        for w in range(W):
+            st.generation(w + 1, workers=workers)
+        t0 = time.perf_counter()
+        for k in range(K):
+            st.generation(W + k + 1, workers=workers)
+        dt = time.perf_counter() - t0
+        sample = (f"each step = one generation of the oracle port of gsgp/evolution.py:146-158 "
+                  f"(numpy, {workers} threads; {why}) on {s_tr}+{s_te} cases")
+    if frac < 1.0:
+        sample += f" of the {N}-case workload; value = steps/s x {frac:.6f} (full-generation equivalents)"
     value = K / dt * frac
-    sample = (f"each step = one reference generation (oracle port of gsgp/evolution.py:146-158, "
-              f"numpy, {workers} threads) over a {s_tr}+{s_te}-case sample of the {N}-case "
-              f"workload; value = steps/s x {frac:.6f} (full-generation equivalents)")
     line = {"metric": METRIC, "value": value, "unit": "generations/s", "n_gpus": world,
             "steps": K, "warmup": W, "ms_per_step": dt / K * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": c["desc"], "m": c["m"], "r": c["r"], "k": c["k"],
-                       "features": c["l"], "n_train": c["ntr"], "n_test": c["nte"]},
+            "config": workload_config(c),
             "impl": "reference",
-            "cpu_baseline": {"value": value, "unit": METRIC, "cores": workers, "kind": "port",
+            "cpu_baseline": {"value": value, "unit": METRIC, "cores": workers, "kind": kind,
                              "sample": sample, "cpu": cpu_bench.cpu_model()},
             "e2e": {"value": value, "unit": METRIC, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
