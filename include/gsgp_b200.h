@@ -148,6 +148,17 @@ int gsgp_gsm(const double* parent, int64_t m, int64_t n, const double* trees, in
              const int64_t* u, const int64_t* v, const double* ms, int32_t sign,
              int32_t squashed, double* out, int64_t* overflow);
 
+/* replay_lineage (gsgp/evolution.py:182-202) on the device: the initial
+ * semantics [m][n] and the raw tree semantics [r][n] are uploaded once, the
+ * g plans (u, v, ms: [g][m]) once, the trees squashed once, then every
+ * generation's fp64 GSM (mutation.py:65-94) and parent-elite restore run on
+ * the device; out[n] = the final elite row (slot final_slot).  elite_src: 0
+ * parent, 1 offspring, per generation. */
+int gsgp_replay(const double* initial, int64_t m, int64_t n, const double* trees, int64_t r, int64_t g,
+                const int64_t* u, const int64_t* v, const double* ms, const int8_t* elite_src,
+                const int64_t* elite_idx, const int64_t* elite_slot, int64_t final_slot, int32_t sign,
+                double* out);
+
 /* The engine's fused fp32 generation step on explicit inputs (kernel-level
  * parity): offspring (fp32, in the engine's rounding) and per-row fp64 SSE. */
 int gsgp_gsm_step_f32(const float* parent_tr, const float* parent_te, const float* sq_tr,

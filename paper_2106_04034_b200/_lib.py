@@ -31,7 +31,7 @@ EXPORTS = (
     "gsgp_comm_unique_id", "gsgp_comm_init", "gsgp_comm_init_host", "gsgp_comm_destroy",
     "gsgp_shard_range",
     "gsgp_sigmoid", "gsgp_argminmax", "gsgp_canonical_sum",
-    "gsgp_init", "gsgp_finalize", "gsgp_device_count_in_use",
+    "gsgp_init", "gsgp_finalize", "gsgp_device_count_in_use", "gsgp_replay",
 )
 
 
@@ -97,6 +97,7 @@ _SIGS = {
     "gsgp_argminmax": (C.c_int, [P, I64, P]),
     "gsgp_canonical_sum": (C.c_int, [P, I64, I64, I32, P]),
     "gsgp_init": (C.c_int, [C.c_int, P]),
+    "gsgp_replay": (C.c_int, [P, I64, I64, P, I64, I64, P, P, P, P, P, P, I64, I32, P]),
     "gsgp_finalize": (C.c_int, []),
     "gsgp_device_count_in_use": (C.c_int, []),
 }

@@ -1,6 +1,7 @@
 // extern "C" boundary (include/gsgp_b200.h).  Each entry point replaces one
 // function of the reference package and runs its sm_100a kernel; errors are
 // returned as status codes with a thread-local message.
+#include <algorithm>
 #include <cstring>
 #include <new>
 #include <string>
@@ -23,6 +24,8 @@ void comm_init(int, int, const unsigned char*);
 void comm_destroy();
 void comm_init_host(int world, int rank, void (*fn)(void*, int64_t, int32_t));
 void trim_device_memory();
+void* cache_alloc(size_t bytes, size_t* got);
+void cache_park(void* p, size_t bytes);
 void devices_init(int, const int*);
 void devices_finalize();
 int devices_count();
@@ -58,18 +61,23 @@ void require_device() {
   }
 }
 
-// RAII device buffer for the operator entry points
+// RAII device buffer for the operator entry points, taken from the engine's
+// device block cache (engine.cu) so repeated operator calls of similar sizes
+// neither cudaMalloc nor cudaFree; the operators run on the legacy default
+// stream, which is drained before a block is parked again
 struct Buf {
   void* p = nullptr;
-  explicit Buf(size_t bytes) {
-    cudaError_t e = cudaMalloc(&p, bytes ? bytes : 16);
-    if (e != cudaSuccess) {
+  size_t bytes = 0;
+  explicit Buf(size_t n) { p = cache_alloc(n ? n : 16, &bytes); }
+  ~Buf() {
+    if (!p) return;
+    if (cudaStreamSynchronize(0) == cudaSuccess) {
+      cache_park(p, bytes);
+    } else {
       cudaGetLastError();
-      throw Error{e == cudaErrorMemoryAllocation ? ERR_OOM : ERR_CUDA,
-                  std::string("cudaMalloc: ") + cudaGetErrorString(e)};
+      cudaFree(p);
     }
   }
-  ~Buf() { if (p) cudaFree(p); }
   Buf(const Buf&) = delete;
   Buf& operator=(const Buf&) = delete;
   template <typename T> T* as() const { return reinterpret_cast<T*>(p); }
@@ -327,6 +335,76 @@ int gsgp_gsm(const double* parent, int64_t m, int64_t n, const double* trees, in
     unsigned long long c = 0;
     d2h(&c, nf.p, 8);
     if (overflow) *overflow += (int64_t)c;
+  });
+}
+
+int gsgp_replay(const double* initial, int64_t m, int64_t n, const double* trees, int64_t r, int64_t g,
+                const int64_t* u, const int64_t* v, const double* ms, const int8_t* elite_src,
+                const int64_t* elite_idx, const int64_t* elite_slot, int64_t final_slot, int32_t sign,
+                double* out) {
+  return guarded([&] {
+    require_device();
+    GSGP_REQUIRE(m >= 1 && n >= 1 && r >= 1 && g >= 0, "empty replay operands");
+    GSGP_REQUIRE(final_slot >= 0 && final_slot < m, "final elite slot out of range");
+    for (int64_t e = 0; e < g * m; ++e) {   // MutationPlan.validate per generation (core.py:213-223)
+      GSGP_REQUIRE(u[e] >= 0 && u[e] < r, "plan index u out of range");
+      GSGP_REQUIRE(v[e] >= 0 && v[e] < r, "plan index v out of range");
+      GSGP_REQUIRE(u[e] != v[e], "plan requires distinct tree indices per slot");
+    }
+    for (int64_t t = 0; t < g; ++t)
+      if (elite_src[t] == 0)
+        GSGP_REQUIRE(elite_idx[t] >= 0 && elite_idx[t] < m && elite_slot[t] >= 0 && elite_slot[t] < m,
+                     "elite record index/slot out of range");
+    const int64_t pitch = pad32(n);
+    Buf P(m * pitch * 8), T(r * pitch * 8), y(pitch * 8), nf(8), e0(pitch * 8), e1(pitch * 8), keep(pitch * 8);
+    Buf du(std::max<int64_t>(g, 1) * m * 8), dv(std::max<int64_t>(g, 1) * m * 8), dm(std::max<int64_t>(g, 1) * m * 8);
+    GSGP_CUDA(cudaMemset(P.p, 0, m * pitch * 8));
+    GSGP_CUDA(cudaMemset(T.p, 0, r * pitch * 8));
+    GSGP_CUDA(cudaMemset(y.p, 0, pitch * 8));
+    GSGP_CUDA(cudaMemset(nf.p, 0, 8));
+    GSGP_CUDA(cudaMemcpy2D(P.p, pitch * 8, initial, n * 8, n * 8, m, cudaMemcpyHostToDevice));
+    GSGP_CUDA(cudaMemcpy2D(T.p, pitch * 8, trees, n * 8, n * 8, r, cudaMemcpyHostToDevice));
+    // gsm() squashes the raw trees every generation (mutation.py:89-94); the
+    // sigmoid is a pure function of the same values, so once is the same bits
+    k_sigmoid<<<nb(r * n), 256>>>(T.as<double>(), r, n, pitch);
+    GSGP_CUDA(cudaGetLastError());
+    if (g > 0) {
+      h2d(du.p, u, g * m * 8);
+      h2d(dv.p, v, g * m * 8);
+      h2d(dm.p, ms, g * m * 8);
+    }
+    const RowLayout lay = make_layout(n, 0, true);
+    Buf part(m * lay.ntiles * 2 * 8), ticket(16);
+    GSGP_CUDA(cudaMemset(ticket.p, 0, 16));
+    GsmArgs a{};
+    a.pool = T.p;
+    a.S = P.p;
+    a.elite_prev = e0.p;
+    a.elite_cur = e1.p;
+    a.y = y.as<double>();
+    a.lay = lay;
+    a.m = m;
+    a.ctl = nullptr;
+    a.sign = sign;
+    a.part = part.as<double>();
+    a.nonfinite = nf.as<unsigned long long>();
+    a.ticket = ticket.as<unsigned long long>();
+    double* S = P.as<double>();
+    // evolution.py:195-201 on the device, in place: offspring = gsm(current);
+    // a parent-sourced elite puts current[index] into offspring[slot], so
+    // that row is saved before the update overwrites it
+    for (int64_t t = 0; t < g; ++t) {
+      const bool parent = elite_src[t] == 0;
+      if (parent)
+        GSGP_CUDA(cudaMemcpyAsync(keep.p, S + elite_idx[t] * pitch, n * 8, cudaMemcpyDeviceToDevice, 0));
+      a.u = du.as<int64_t>() + t * m;
+      a.v = dv.as<int64_t>() + t * m;
+      a.ms = dm.as<double>() + t * m;
+      launch_gsm(a, true, true, 0);
+      if (parent)
+        GSGP_CUDA(cudaMemcpyAsync(S + elite_slot[t] * pitch, keep.p, n * 8, cudaMemcpyDeviceToDevice, 0));
+    }
+    d2h(out, S + final_slot * pitch, n * 8);
   });
 }
 

@@ -99,6 +99,14 @@ void* cache_alloc(size_t bytes, size_t* got) {
   return p;
 }
 
+// return a block to the cache (its last use must be complete)
+void cache_park(void* p, size_t bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  g_cache.push_back({p, bytes, dev});
+}
+
 thread_local cudaStream_t g_alloc_stream = nullptr;   // stream a released block may still be used on
 
 struct DevBuf {

@@ -153,19 +153,32 @@ def run_evolution(cfg: RunConfig, train: Dataset, test: Dataset, *, storage: str
 
 def replay_lineage(log: LineageLog, initial_semantics: np.ndarray, tree_semantics: np.ndarray,
                    cfg: RunConfig) -> np.ndarray:
-    """gsgp/evolution.py:182-202: re-apply every plan and survival decision
-    with the device fp64 GSM (sigmoid recomputed each generation, as in the
-    reference), returning the final elite's semantics."""
+    """gsgp/evolution.py:182-202 in ONE device call (`gsgp_replay`): the
+    initial and tree semantics and all plans are uploaded once, every
+    generation's fp64 GSM (sigmoid of the trees, as in the reference's gsm)
+    and parent-elite restore run on the device, and only the final elite row
+    comes back."""
     if log.generations != cfg.generations:
         raise LineageError(
             f"log covers {log.generations} generations, config expects {cfg.generations}")
-    m = initial_semantics.shape[0]
-    cur = np.array(initial_semantics, dtype=np.float64, copy=True)
+    cur = np.ascontiguousarray(initial_semantics, dtype=np.float64)
+    trees = np.ascontiguousarray(tree_semantics, dtype=np.float64)
+    if cur.ndim != 2 or trees.ndim != 2 or cur.shape[1] != trees.shape[1]:
+        raise ConfigError("parent and random-tree matrices must share the case axis")
+    m, n = cur.shape
+    g = len(log.entries)
     for entry in log.entries:
         if len(entry.plan) != m:
             raise LineageError("plan length does not match the population size")
-        nxt = ops.gsm(cur, tree_semantics, entry.plan, cfg)
-        if entry.elite.source == "parent":
-            nxt[entry.elite.slot] = cur[entry.elite.index]
-        cur = nxt
-    return cur[log.final_elite().slot].copy()
+    shape = (max(g, 1), m)
+    u, v, ms = np.zeros(shape, np.int64), np.zeros(shape, np.int64), np.zeros(shape)
+    src, idx, slot = np.ones(max(g, 1), np.int8), np.zeros(max(g, 1), np.int64), np.zeros(max(g, 1), np.int64)
+    for t, e in enumerate(log.entries):
+        u[t], v[t], ms[t] = e.plan.u, e.plan.v, e.plan.ms
+        src[t] = 0 if e.elite.source == "parent" else 1
+        idx[t], slot[t] = e.elite.index, e.elite.slot
+    out = np.empty(n)
+    check(_lib.load().gsgp_replay(ptr(cur), m, n, ptr(trees), trees.shape[0], g, ptr(u), ptr(v), ptr(ms),
+                                  ptr(src), ptr(idx), ptr(slot), int(log.final_elite().slot),
+                                  1 if cfg.gsm_sign == "plus" else 0, ptr(out)))
+    return out

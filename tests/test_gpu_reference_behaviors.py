@@ -65,6 +65,44 @@ def test_replay_empty_and_truncated_logs():
         G.replay_lineage(truncated, *_initial(cfg6, train), cfg6)
 
 
+@pytest.mark.parametrize("name", ["plus", "accept", "c1"])
+def test_device_replay_reproduces_reference_elite_of_golden_runs(name):
+    """gsgp_replay (one device call: plans uploaded once, fp64 GSM and elite
+    restores on the device) on the REFERENCE's lineage reproduces the
+    reference's final elite semantics bit for bit (the reference's own
+    replay contract, pkg/tests/test_evolution.py:197-217)."""
+    import ast
+    from conftest import golden
+    g = golden(f"run_{name}")
+    if "u" not in g.files:
+        pytest.skip("golden without stored plans")
+    cfg = RunConfig(**ast.literal_eval(str(g["cfg"][0])))
+    train = G.Dataset(g["Xtr"], g["ytr"])
+    log = G.LineageLog(G.EliteRecord("initial", int(g["init"][0]), int(g["init"][0]), float(g["init_fit"][0])))
+    for t in range(cfg.generations):
+        src = "parent" if g["src"][t] == 0 else "offspring"
+        log.entries.append(G.LineageEntry(G.MutationPlan(g["u"][t], g["v"][t], g["ms"][t]),
+                                          G.EliteRecord(src, int(g["idx"][t]), int(g["slot"][t]),
+                                                        float(g["fit"][t]))))
+    replayed = G.replay_lineage(log, *_initial(cfg, train), cfg)
+    assert np.array_equal(replayed, g["elite_sem"])
+
+
+def test_device_replay_validates_plans_like_the_reference():
+    cfg = RunConfig(population_size=4, random_trees=3, program_size=9, generations=2, seed=3)
+    train, test = _ds(6, 2, 21), _ds(3, 2, 22)
+    res = G.run_evolution(cfg, train, test, storage="fp64")
+    init, trees = _initial(cfg, train)
+    bad = dataclasses.replace(res.lineage)
+    bad.entries = list(res.lineage.entries)
+    e = bad.entries[1]
+    bad.entries[1] = G.LineageEntry(G.MutationPlan(e.plan.v, e.plan.v, e.plan.ms), e.elite)   # u == v
+    with pytest.raises(ConfigError):
+        G.replay_lineage(bad, init, trees, cfg)
+    with pytest.raises(ConfigError):
+        G.replay_lineage(res.lineage, init, trees[:, :-1], cfg)
+
+
 def test_gsm_every_slot_mutated_and_timings():
     # pkg/tests/test_evolution.py:180-195 and :256-262
     cfg = RunConfig(population_size=16, random_trees=8, program_size=15, generations=4, seed=9)
