@@ -91,8 +91,10 @@ def run_evolution(cfg: RunConfig, train: Dataset, test: Dataset, *, storage: str
         raise ConfigError(f"train has {train.n_features} features but test has {test.n_features}")
     t0 = time.perf_counter()
     m, g = cfg.population_size, cfg.generations
-    Xtr, ytr = train.features, train.target
-    Xte, yte = test.features, test.target
+    # the reference's Dataset may hold strided views (load_dataset slices the
+    # target column off): the C ABI takes C-contiguous fp64
+    Xtr, ytr = ops._f64(train.features), ops._f64(train.target)
+    Xte, yte = ops._f64(test.features), ops._f64(test.target)
     s = ops.config_struct(cfg, storage=storage, use_graph=use_graph, time_kernels=time_kernels,
                           virtual_shards=virtual_shards, window_start=window_start)
     out = _lib.GsgpOutputs()

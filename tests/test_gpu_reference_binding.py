@@ -4,7 +4,8 @@
 `gsgp/_cuda.py` — evolution.py:100, the CLI `-backend` choices — io_cli.py:259,
 `_effective_workers` — harness.py:44-47) is applied to a temp copy of the
 UNMODIFIED reference in baseline/_ref, and the reference's OWN run-level
-tests run against it with every RunConfig forced to backend "cuda":
+tests run against it with GSGP_BACKEND=cuda (the patch's environment
+override: every run_evolution call of those tests executes on the device):
 pkg/tests/test_evolution.py (run determinism, monotonicity, traces,
 backend agreement, replay), test_io_cli.py (full CLI runs, byte-identical
 outputs across seeds/backends/runs), test_harness.py (timed_run / sweep /
@@ -47,22 +48,11 @@ ALLOWED_FAILURES = {
         "numpy fp64 replay and numpy cumsum RMSE of an fp32-storage device run",
     "test_acceptance.py::test_replay_fidelity":
         "numpy fp64 replay of an fp32-storage device run",
+    "test_evolution.py::test_replay_empty_log_returns_initial_elite":
+        "fp32-stored initial elite vs fp64 numpy semantics; numpy cumsum RMSE vs the canonical SSE",
+    "test_io_cli.py::test_sidecar_replay_reproduces_final_trace_value":
+        "numpy cumsum RMSE of a numpy fp64 replay vs the device trace, compared with ==",
 }
-
-PLUGIN = '''
-"""pytest plugin: every RunConfig the reference's tests build runs on the device."""
-import gsgp.core as _core
-
-_orig = _core.RunConfig.__post_init__
-
-
-def _post_init(self):
-    object.__setattr__(self, "backend", "cuda")
-    _orig(self)
-
-
-_core.RunConfig.__post_init__ = _post_init
-'''
 
 FILES = ["test_evolution.py", "test_io_cli.py", "test_harness.py", "test_acceptance.py"]
 # acceptance criteria that need the absent yacht/tower data, or that time the
@@ -83,7 +73,6 @@ def patched(tmp_path_factory):
     shutil.copytree(REF / "ref_tests", d / "tests", ignore=shutil.ignore_patterns("__pycache__", ".hypothesis"))
     r = subprocess.run(["patch", "-p1", "-i", str(PATCH)], cwd=d, capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr
-    (d / "gsgp_cuda_plugin.py").write_text(PLUGIN)
     return d
 
 
@@ -105,9 +94,9 @@ def test_patch_applies_and_binds_the_device_engine(patched):
 
 
 def test_reference_run_level_tests_pass_on_the_device(patched):
-    env = dict(os.environ, PYTHONPATH=f"{patched}{os.pathsep}{patched / 'tests'}{os.pathsep}{ROOT}")
-    args = [sys.executable, "-m", "pytest", "-p", "gsgp_cuda_plugin", "-p", "no:cacheprovider", "-q", "-rfE",
-            "--timeout=900"]
+    env = dict(os.environ, PYTHONPATH=f"{patched}{os.pathsep}{patched / 'tests'}{os.pathsep}{ROOT}",
+               GSGP_BACKEND="cuda")
+    args = [sys.executable, "-m", "pytest", "-p", "no:cacheprovider", "-q", "-rfE", "--timeout=900"]
     for t in DESELECT:
         args += ["--deselect", f"tests/{t}"]
     args += [f"tests/{f}" for f in FILES]
@@ -118,4 +107,4 @@ def test_reference_run_level_tests_pass_on_the_device(patched):
     passed = int(m.group(1)) if m else 0
     unexpected = {f for f in failed if f.split("[")[0] not in ALLOWED_FAILURES}
     assert not unexpected, text[-6000:]
-    assert passed >= 40, text[-3000:]
+    assert passed >= 50, text[-3000:]
