@@ -209,14 +209,14 @@ int gsgp_compute_semantics(const uint8_t* tags, const int32_t* codes, const doub
     h2d(dc.p, codes, count * k * 4);
     h2d(dv.p, consts, count * k * 8);
     Buf ins(count * (k + 1) * sizeof(Ins)), exe(kMaxInterpGroups * count * (k + 1) * sizeof(Ins)), len(count * 4),
-        nconst(count * 4), ctab(count * k * 8), mx(3 * 4), scr(count * 4 * k * 4), fl(count * k),
+        nconst(count * 4), ctab(count * k * 8), mx(4 * 4), scr(count * 4 * k * 4), fl(count * k),
         cv(count * k * 8);
     Program prog{ins.as<Ins>(), exe.as<Ins>(), len.as<int32_t>(), nconst.as<int32_t>(),
                  ctab.as<double>(), mx.as<int32_t>(), scr.as<int32_t>(), fl.as<uint8_t>(),
                  cv.as<double>()};
     launch_compile(dt.as<uint8_t>(), dc.as<int32_t>(), dv.as<double>(), count, (int32_t)k, eps, prog, 0);
-    int32_t maxima[3] = {0, 0, 0};
-    d2h(maxima, mx.p, 12);
+    int32_t maxima[4] = {0, 0, 0, 0};
+    d2h(maxima, mx.p, 16);
     Buf xr(n * l * 8), xt(n * l * 8), o(count * n * 8), nf(8);
     h2d(xr.p, X, n * l * 8);
     k_transpose_op<<<nb(n * l), 256>>>(xr.as<double>(), n, l, xt.as<double>());
@@ -243,6 +243,7 @@ int gsgp_compute_semantics(const uint8_t* tags, const int32_t* codes, const doub
     a.maxdepth = maxima[0];
     a.maxconst = maxima[1];
     a.maxlen = maxima[2];
+    a.maxwords = maxima[3];
     a.out64 = o.as<double>();
     a.nonfinite = nf.as<unsigned long long>();
     a.raw = replace_nonfinite ? 0 : 1;

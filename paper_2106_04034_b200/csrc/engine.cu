@@ -539,7 +539,7 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   plen.alloc(ng * 4);
   pnconst.alloc(ng * 4);
   ctab.alloc(ng * k * 8);
-  pmax.alloc(3 * 4);
+  pmax.alloc(4 * 4);
   scratch.alloc(ng * 4 * k * 4);
   flags.alloc(ng * k);
   cval.alloc(ng * k * 8);
@@ -581,8 +581,8 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   launch_compile(tags.as<uint8_t>(), codes.as<int32_t>(), consts.as<double>(), ng, (int32_t)k,
                  cfg->division_eps, prog, st);
   GSGP_CUDA(cudaEventRecord(ev_compile1.e, st));
-  int32_t maxima[3] = {0, 0, 0};   // {spill depth, constants, instructions}
-  GSGP_CUDA(cudaMemcpyAsync(maxima, pmax.p, 12, cudaMemcpyDeviceToHost, st));
+  int32_t maxima[4] = {0, 0, 0, 0};   // {spill depth, constants, instructions, RF words}
+  GSGP_CUDA(cudaMemcpyAsync(maxima, pmax.p, 16, cudaMemcpyDeviceToHost, st));
   // program lengths: one instruction per function node of the compiled tree
   // (the interpreter's work unit, reported as node evaluations per second)
   std::vector<int32_t> hlen(ng);
@@ -632,6 +632,7 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
     ia.maxdepth = maxima[0];
     ia.maxconst = maxima[1];
     ia.maxlen = maxima[2];
+    ia.maxwords = maxima[3];
     ia.out = p->S.p;
     ia.out_is_f64 = f64 ? 1 : 0;
     ia.pitch = p->pitch;

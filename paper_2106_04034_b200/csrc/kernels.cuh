@@ -59,7 +59,8 @@ struct Program {
   int32_t* len;         // [count] instructions
   int32_t* nconst;      // [count] constant-table entries
   double* ctab;         // [count][k] constants referenced by the program
-  int32_t* maxima;      // [3] {spill depth, constants, instructions}: max over genomes
+  int32_t* maxima;      // [4] {spill depth, constants, instructions, register-feature
+                        // program words (interp_rf_dispatch.inc)}: max over genomes
   int32_t* scratch;     // [count][4*k] ints
   uint8_t* flags;       // [count][k]
   double* cval;         // [count][k]
@@ -82,6 +83,7 @@ struct InterpArgs {
   int64_t k1;               // instruction stride per genome (k + 1)
   int64_t count;            // genomes
   int32_t maxdepth, maxconst, maxlen;   // Program::maxima, read back once after compile
+  int32_t maxwords;                     // Program::maxima[3]
   const double* XT;         // [l][xt_pitch] fp64, feature-major: cases q_base .. q_base+nq-1
   int64_t xt_pitch;
   int32_t l;

@@ -409,7 +409,7 @@ def test_interpreter_division_fast_path_near_halfway_quotients():
     ref, _ = R.semantics(tags, codes, consts, X, 1e-6)
     pop = Population(tags, codes, consts)
     import os
-    for cfg in ("0", "1", "2", "3", "4", "5", "6", "7"):
+    for cfg in ("0", "1", "2", "3", "4", "5", "6", "7", "8"):
         os.environ["GSGP_INTERP_CFG"] = cfg
         try:
             S = G.compute_semantics(pop, X, RunConfig(program_size=k))
@@ -432,7 +432,7 @@ def test_dataset_split_matches_reference_golden():
 
 
 @pytest.mark.parametrize("count", [1, 2, 3, 5, 17])
-@pytest.mark.parametrize("cfg", ["5", "6", "7"])
+@pytest.mark.parametrize("cfg", ["5", "6", "7", "8"])
 def test_interpreter_genome_groups_with_odd_counts(count, cfg, monkeypatch):
     """Grouped interpreter blocks (cfg 6: two genome groups of 128 threads
     per block sharing the feature tile) with genome counts that leave a
@@ -446,3 +446,52 @@ def test_interpreter_genome_groups_with_odd_counts(count, cfg, monkeypatch):
     monkeypatch.setenv("GSGP_INTERP_CFG", cfg)
     S = G.compute_semantics(pop, X, cfg_run)
     assert np.array_equal(S.view(np.uint64), ref.view(np.uint64))
+
+
+@pytest.mark.parametrize("cfg", ["8", "5"])
+def test_interpreter_divisions_by_and_of_constants_and_spills(cfg, monkeypatch):
+    """Register-feature arms (interp_rf_dispatch.inc): a constant numerator or
+    denominator takes a static range test (in-range constants use the fast
+    path, out-of-range ones — 0, subnormal, tiny, huge, inf, near eps — the
+    always-slow arms), a spill operand the dynamic one; every result must be
+    bit-exact with numpy, guard included (gsgp/interpreter.py:58-65)."""
+    rng = np.random.default_rng(21)
+    n = 3000
+    X = np.stack([_hard_division_operands(rng, n), _hard_division_operands(rng, n),
+                  rng.uniform(-3, 3, n)], axis=1)
+    X[::17, 0] = 0.0
+    X[::23, 1] = 5e-7                      # below eps: guard
+    X[::29, 2] = 2e-6                      # just above eps
+    F, V, C_, DIV = int(GeneTag.FUNCTION), int(GeneTag.FEATURE), int(GeneTag.CONSTANT), int(FunctionOp.DIV)
+    cvals = [0.0, 5e-324, 1e-300, 5e-7, 2e-6, 3.5, -2.0 ** 500, 1e300, float("inf"), -7.25e-151]
+    progs = []
+    for c in cvals:
+        progs.append([(V, 0), (C_, c), (F, DIV)])                      # x0 / c
+        progs.append([(C_, c), (V, 1), (F, DIV)])                      # c / x1
+        progs.append([(V, 0), (V, 2), (F, int(FunctionOp.MUL)), (C_, c), (F, DIV)])    # (x0*x2) / c
+        progs.append([(C_, c), (V, 0), (V, 1), (F, int(FunctionOp.SUB)), (F, DIV)])    # c / (x0-x1)
+    # spill operands: (x0/x1) / (x1/x2), (x0*x2 - x1) / (x2 + x0 / x1)
+    progs.append([(V, 0), (V, 1), (F, DIV), (V, 1), (V, 2), (F, DIV), (F, DIV)])
+    progs.append([(V, 0), (V, 2), (F, int(FunctionOp.MUL)), (V, 1), (F, int(FunctionOp.SUB)),
+                  (V, 2), (V, 0), (V, 1), (F, DIV), (F, int(FunctionOp.ADD)), (F, DIV)])
+    k = max(len(p) for p in progs)
+    tags = np.full((len(progs), k), C_, np.uint8)
+    codes = np.zeros((len(progs), k), np.int32)
+    consts = np.full((len(progs), k), 1.0)
+    for i, p in enumerate(progs):
+        off = k - len(p)
+        for jj, (t, c) in enumerate(p):
+            tags[i, off + jj] = t
+            if t == C_:
+                consts[i, off + jj] = c
+            else:
+                codes[i, off + jj] = c
+    pop = Population(tags, codes, consts)
+    monkeypatch.setenv("GSGP_INTERP_CFG", cfg)
+    for eps in (1e-6, 1e-9):
+        with np.errstate(all="ignore"):
+            ref, _ = R.semantics(tags, codes, consts, X, eps)
+        S = G.compute_semantics(pop, X, RunConfig(program_size=k, division_eps=eps))
+        ok = np.isfinite(ref)
+        assert np.array_equal(S[ok].view(np.uint64), ref[ok].view(np.uint64)), (cfg, eps)
+        assert np.all(S[~ok] == 0.0)
