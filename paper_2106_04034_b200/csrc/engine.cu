@@ -852,9 +852,11 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   DevBuf gemax;
   gemax.alloc(m * 2 * 4);
   GSGP_CUDA(cudaMemsetAsync(gemax.p, 0x80, m * 2 * 4, st));
-  // one generation: GSM+SSE with the plan drawn inline (per shard), then the
-  // canonical SSE and survival — fused into one kernel when there is a
-  // single shard, else anchors / digits per shard -> allreduce -> finish -> survive
+  GSGP_CUDA(cudaMemsetAsync(cdig.p, 0, m * 2 * kLimbs * 8, st));   // digit sums of the sharded tail
+  // one generation: GSM+SSE with the plan drawn inline (per shard; every
+  // launch accumulates the canonical-sum anchors), then the canonical SSE and
+  // survival — one kernel when there is a single shard, else digits per
+  // shard (between the two allreduces) and one finish + survive kernel
   auto enqueue_generation = [&](cudaStream_t s, Event* t0, Event* t1) {
     int64_t n = 0;
     if (t0) GSGP_CUDA(cudaEventRecord(t0->e, s));
@@ -877,7 +879,9 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
       a.sign = cfg->gsm_sign;
       a.part = p->part.as<double>();
       a.ticket = p->ticket.as<unsigned long long>();
-      a.emax = (fused_tail && p->ntiles > 1) ? gemax.as<int32_t>() : nullptr;   // single unit: SSE = partial
+      // anchors: every shard of the sharded tail; the fused tail only when a
+      // row has several units (single unit: SSE = partial)
+      a.emax = (!fused_tail || p->ntiles > 1) ? gemax.as<int32_t>() : nullptr;
       a.plan_inline = 1;
       a.write_plan = plan_written ? 0 : 1;   // the first non-empty shard records the plan
       plan_written = true;
@@ -895,10 +899,18 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
                             done.as<unsigned int>(), s);
       ++n;
     } else {
-      canon_sse(false, sse_vec, s);
-      for (auto& p : sh) n += p->pitch > 0 ? 2 : 0;   // exp + digits per non-empty shard
-      ++n;                                             // finish
-      launch_survive(sa, s);
+      // GSM (anchors) -> allreduce-max -> digits per shard -> allreduce-sum
+      // -> finish + survive (re-arms anchors and digits)
+      if (coll) allreduce(gemax.p, m * 2, kRedI32Max, s, "ncclAllReduce(sse anchors)");
+      for (auto& p : sh) {
+        if (p->pitch == 0) continue;
+        launch_canon_digits(p->part.as<double>(), m, p->ntiles, gemax.as<int32_t>(),
+                            cdig.as<unsigned long long>(), s);
+        ++n;
+      }
+      if (coll) allreduce(cdig.p, m * 2 * kLimbs, kRedU64Sum, s, "ncclAllReduce(sse digits)");
+      launch_finish_survive(gemax.as<int32_t>(), cdig.as<unsigned long long>(), sse_vec, sa,
+                            done.as<unsigned int>(), s);
       ++n;
     }
     launches_per_gen = n;

@@ -256,8 +256,10 @@ int choose_cfg(const InterpArgs& a) {
   if (forced >= 0 && forced < kNumCfgs && cfg_smem(kCfgs[forced], a) <= kSmemCap &&
       (kCfgs[forced].groups == 1 || a.exe_gstride > 0) && (!kCfgs[forced].rf || rf_ok))
     return forced;
-  // features in registers whenever the dataset has at most 8 of them
-  if (rf_ok && !getenv("GSGP_INTERP_NO_RF")) return kCfgRf;
+  // the register-feature interpreter (kCfgRf) is opt-in only: measured
+  // slower than the grouped shared-memory tiles at C2/C3 (C3 pop + pool
+  // 2224 vs 1768 ms, C2 13.7 vs 10.0 ms per launch: profiles/r02/README.md)
+  if (rf_ok && getenv("GSGP_INTERP_RF")) return kCfgRf;
   // two genome groups of 128 x 4 per block (cfg 7, compiled for 3 resident
   // blocks = 24 warps) when shared memory keeps 3 of them per SM: measured
   // 2.8 % faster at C3 than 128 x 3 groups with 32 warps (more cases per

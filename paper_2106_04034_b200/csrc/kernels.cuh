@@ -206,13 +206,17 @@ struct SurviveArgs {
   int8_t* rec_src; int64_t* rec_idx; int64_t* rec_slot; double* rec_fit;
   double* trace_tr; double* trace_te;
 };
-void launch_survive(const SurviveArgs& a, cudaStream_t s);
 // per-row canonical SSE into sse (== a.sse_off) fused with survival (single
 // shard, single rank); emax = the anchors the GSM launch accumulated (reset
 // to kExpZero here; unused when ntiles == 1: the SSE is the partial itself);
 // `done` is a zeroed counter, re-zeroed on exit
 void launch_reduce_survive(const double* part, int64_t ntiles, int32_t* emax, double* sse,
                            const SurviveArgs& a, unsigned int* done, cudaStream_t s);
+// multi-shard / multi-rank tail: sse = canon_finish(digits, emax) per (row,
+// train|test), emax re-armed to kExpZero and digits zeroed for the next
+// generation, then survival in the last block (`done` as above)
+void launch_finish_survive(int32_t* emax, unsigned long long* digits, double* sse, const SurviveArgs& a,
+                           unsigned int* done, cudaStream_t s);
 // initial elite: fitness from SSE, argmin, trace[0] (evolution.py:132-143)
 void launch_init_state(const SurviveArgs& a, cudaStream_t s);
 // decision only, for the operator API: out = {src, idx, slot}

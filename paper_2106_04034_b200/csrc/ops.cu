@@ -406,8 +406,6 @@ __device__ void survive_block(const SurviveArgs& a) {
   }
 }
 
-__global__ void __launch_bounds__(1024) k_survive(SurviveArgs a) { survive_block(a); }
-
 // Canonical SSE of every row (one warp per row, warp_row_sse above) fused
 // with survival: the last block to finish runs survive_block.
 template <int kPer>
@@ -417,6 +415,37 @@ __global__ void __launch_bounds__(256) k_reduce_survive(const double* __restrict
   __shared__ int last;
   const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (row < a.m) warp_row_sse_anchored<kPer>(part, ntiles, row, emax, sse);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  survive_block(a);
+  if (threadIdx.x == 0) *done = 0;
+}
+
+// multi-shard / multi-rank generation tail, after the GSM launches
+// accumulated the anchors (emax, allreduce-max over ranks) and k_canon_digits
+// the digit sums (allreduce-sum over ranks): one rounding per (row,
+// train|test), both accumulators re-armed for the next generation, and the
+// last block runs the survival.
+__global__ void __launch_bounds__(256) k_finish_survive(int32_t* emax, unsigned long long* digits,
+                                                        double* __restrict__ sse, SurviveArgs a,
+                                                        unsigned int* done) {
+  __shared__ int last;
+  const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;   // (row, train|test)
+  if (i < 2 * a.m) {
+    unsigned long long L[kLimbs];
+    unsigned long long* d = digits + (i >> 1) * 2 * kLimbs + (i & 1) * kLimbs;
+#pragma unroll
+    for (int j = 0; j < kLimbs; ++j) {
+      L[j] = d[j];
+      d[j] = 0;
+    }
+    sse[i] = canon_finish(L, emax[i]);
+    emax[i] = kExpZero;
+  }
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
@@ -612,8 +641,9 @@ void launch_reduce_survive(const double* part, int64_t ntiles, int32_t* emax, do
   check_launch();
 }
 
-void launch_survive(const SurviveArgs& a, cudaStream_t s) {
-  k_survive<<<1, 1024, 0, s>>>(a);
+void launch_finish_survive(int32_t* emax, unsigned long long* digits, double* sse, const SurviveArgs& a,
+                           unsigned int* done, cudaStream_t s) {
+  k_finish_survive<<<(unsigned)((2 * a.m + 255) / 256), 256, 0, s>>>(emax, digits, sse, a, done);
   check_launch();
 }
 

@@ -42,10 +42,10 @@ def test_bench_two_ranks_host_exchange():
     d = _torchrun("--gpus", "2", "--config", "c2", "--steps", "5", "--warmup", "3", "--no-cpu-baseline",
                   "--no-secondary", env_extra={"GSGP_BENCH_HOST_EXCHANGE": "1"})
     assert d["n_gpus"] == 2 and d["steps"] == 5 and d["warmup"] == 3
-    assert d["value"] > 0 and d["ms_per_step"] > 0 and d["config"]["parallelism"] == "case-shard x2"
+    assert d["value"] > 0 and d["ms_per_step"] > 0 and d["parallelism"].startswith("case-shard x2")
     assert d["gpu_launches"] > 0 and d["roofline"]["frac"] > 0
 
 
 def test_reference_arm_under_torchrun_prints_once():
     d = _torchrun("--impl", "reference", "--gpus", "2", "--config", "c1", "--steps", "3", "--warmup", "3")
-    assert d["impl"] == "reference" and d["value"] > 0 and d["cpu_baseline"]["kind"] == "port"
+    assert d["impl"] == "reference" and d["value"] > 0 and d["cpu_baseline"]["kind"] in ("reference", "port")
