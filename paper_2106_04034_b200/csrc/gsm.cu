@@ -82,6 +82,9 @@ __device__ __forceinline__ UnitSpan unit_span(int64_t t, const RowLayout& L) {
 #ifndef GSGP_GSM_CWARPS
 #define GSGP_GSM_CWARPS 16
 #endif
+#ifndef GSGP_GSM_TEAMS
+#define GSGP_GSM_TEAMS 1
+#endif
 constexpr int kTileBytes = GSGP_GSM_TILE;
 
 // ===================================================================
@@ -112,6 +115,16 @@ constexpr int kStages = GSGP_GSM_STAGES;
 constexpr int kRedStages = 4;
 constexpr int kConsumerWarps = GSGP_GSM_CWARPS;
 constexpr int kNCT = kConsumerWarps * 32;
+// consumer teams: the consumer warps split into kTeams teams that take
+// alternate stages, so kTeams units are in flight in the consumers at once;
+// each team thread does the work of kTeams consumer threads of the one-team
+// layout with the same elements and the same summation order (bit-identical
+// SSE partials), keeping kTeams independent chains
+constexpr int kTeams = GSGP_GSM_TEAMS;
+constexpr int kTeamWarps = kConsumerWarps / kTeams;
+constexpr int kTeamThreads = kTeamWarps * 32;
+static_assert(kConsumerWarps % kTeams == 0 && kStages % kTeams == 0 && 4 % kTeams == 0,
+              "teams must divide the consumer warps and both rings");
 constexpr int kTmaThreads = (kConsumerWarps + 2) * 32;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -214,10 +227,10 @@ k_gsm_tma(GsmArgs a, int64_t nunits, int kBatch) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(full + s, 1);
-      mbar_init(empty + s, kConsumerWarps);
+      mbar_init(empty + s, kTeamWarps);
     }
     for (int s = 0; s < kRedStages; ++s) {
-      mbar_init(rfull + s, kConsumerWarps);
+      mbar_init(rfull + s, kTeamWarps);
       mbar_init(rempty + s, 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -296,12 +309,21 @@ k_gsm_tma(GsmArgs a, int64_t nunits, int kBatch) {
         const T* pu = reinterpret_cast<const T*>(__shfl_sync(0xffffffffu, (unsigned long long)pub, q));
         const T* pv = reinterpret_cast<const T*>(__shfl_sync(0xffffffffu, (unsigned long long)pvb, q));
         const double msd = __shfl_sync(0xffffffffu, msb, q);
+        if (unit >= nunits) {   // one terminator per consumer team
+          if (lane == 0)
+            for (int tt = 0; tt < kTeams; ++tt, ++k) {
+              if (k >= kStages) mbar_wait(empty + s, (j & 1) ^ 1);
+              slot_unit[s] = -1;
+              mbar_arrive(full + s);
+              if (++s == kStages) { s = 0; ++j; }
+            }
+          __syncwarp();
+          done = true;
+          break;
+        }
         if (lane == 0) {
           if (k >= kStages) mbar_wait(empty + s, (j & 1) ^ 1);
-          if (unit >= nunits) {
-            slot_unit[s] = -1;
-            mbar_arrive(full + s);
-          } else {
+          {
             const uint32_t bytes = (uint32_t)n * (uint32_t)sizeof(T);
             T* d = data + (int64_t)s * 3 * TILE;
             slot_unit[s] = unit;
@@ -317,7 +339,6 @@ k_gsm_tma(GsmArgs a, int64_t nunits, int kBatch) {
           }
         }
         __syncwarp();
-        if (unit >= nunits) { done = true; break; }
         if (++s == kStages) { s = 0; ++j; }
       }
     }
@@ -362,92 +383,110 @@ k_gsm_tma(GsmArgs a, int64_t nunits, int kBatch) {
   }
 
   // -------------------------------------------------------------- consumers
-  const int ct = threadIdx.x;   // 0 .. kNCT-1
+  // team tm takes the units n = tm, tm + kTeams, ... of this CTA (stage
+  // n % kStages, reduction slot n % kRedStages); team thread tct does the
+  // elements of one-team consumer threads tct + o * kTeamThreads, o < kTeams,
+  // whose warp partials go to slots tw + o * kTeamWarps
+  const int tm = warp / kTeamWarps, tw = warp % kTeamWarps;
+  const int tct = threadIdx.x % kTeamThreads;
   int64_t cur_t = -1;
-  int s = 0, rs = 0;
-  uint32_t j = 0, rj = 0;
-  double y[VPT][EV];
+  double y[kTeams][VPT][EV];
   unsigned long long nonfinite = 0;
-  for (int64_t k = 0;; ++k) {
+  for (int64_t n = tm;; n += kTeams) {
+    const int s = (int)(n % kStages), rs = (int)(n % kRedStages);
+    const uint32_t j = (uint32_t)(n / kStages), rj = (uint32_t)(n / kRedStages);
     mbar_wait(full + s, j & 1);
     const int64_t unit = slot_unit[s];
     if (unit < 0) {   // no more units: tell the finalizer and stop
       if (lane == 0) {
-        if (k >= kRedStages) mbar_wait(rempty + rs, (rj & 1) ^ 1);
-        if (warp == 0) red_unit[rs] = -1;
+        if (n >= kRedStages) mbar_wait(rempty + rs, (rj & 1) ^ 1);
+        if (tw == 0) red_unit[rs] = -1;
         mbar_arrive(rfull + rs);
       }
       break;
     }
     const int4 it = slot_it[s];
     const int64_t t = it.y, i = it.x;
-    const int n = it.z, nA = it.w;                      // elements [0, nA) are train cases
+    const int nn = it.z, nA = it.w;                     // elements [0, nA) are train cases
     const int64_t off = slot_off[s];
-    if (t != cur_t) {   // target tile: registers, reloaded when the CTA changes tile
+    if (t != cur_t) {   // target tile: registers, reloaded when the team changes tile
 #pragma unroll
-      for (int q = 0; q < VPT; ++q) {
-        const int e = (q * kNCT + ct) * EV;
+      for (int o = 0; o < kTeams; ++o)
 #pragma unroll
-        for (int c = 0; c < EV; ++c) y[q][c] = e < n ? __ldg(a.y + off + e + c) : 0.0;
-      }
+        for (int q = 0; q < VPT; ++q) {
+          const int e = (q * kNCT + o * kTeamThreads + tct) * EV;
+#pragma unroll
+          for (int c = 0; c < EV; ++c) y[o][q][c] = e < nn ? __ldg(a.y + off + e + c) : 0.0;
+        }
       cur_t = t;
     }
     const T msv = (T)slot_ms[s];
     const bool save = (i == bp);
     const T* d = data + (int64_t)s * 3 * TILE;
-    Vec P[VPT], A[VPT], B[VPT];
+    Vec P[kTeams][VPT], A[kTeams][VPT], B[kTeams][VPT];
 #pragma unroll
-    for (int q = 0; q < VPT; ++q) {
-      const int e = (q * kNCT + ct) * EV;
-      P[q] = *reinterpret_cast<const Vec*>(d + e);
-      if (!kSseOnly) {
-        A[q] = *reinterpret_cast<const Vec*>(d + TILE + e);
-        B[q] = *reinterpret_cast<const Vec*>(d + 2 * TILE + e);
+    for (int o = 0; o < kTeams; ++o)
+#pragma unroll
+      for (int q = 0; q < VPT; ++q) {
+        const int e = (q * kNCT + o * kTeamThreads + tct) * EV;
+        P[o][q] = *reinterpret_cast<const Vec*>(d + e);
+        if (!kSseOnly) {
+          A[o][q] = *reinterpret_cast<const Vec*>(d + TILE + e);
+          B[o][q] = *reinterpret_cast<const Vec*>(d + 2 * TILE + e);
+        }
       }
-    }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty + s);   // stage free: the producer refills while we compute
-    if (++s == kStages) { s = 0; ++j; }
 
     T* orow = S + i * a.lay.pitch + off;
-    double acc_tr = 0.0, acc_te = 0.0;
+    double acc_tr[kTeams], acc_te[kTeams];
 #pragma unroll
-    for (int q = 0; q < VPT; ++q) {
-      const int e = (q * kNCT + ct) * EV;
-      if (e >= n) continue;
-      const T* pe = reinterpret_cast<const T*>(&P[q]);
-      const T* ae = reinterpret_cast<const T*>(&A[q]);
-      const T* be = reinterpret_cast<const T*>(&B[q]);
-      Vec O;
-      T* oe = reinterpret_cast<T*>(&O);
-      double sacc = 0.0;
+    for (int o = 0; o < kTeams; ++o) {
+      acc_tr[o] = 0.0;
+      acc_te[o] = 0.0;
 #pragma unroll
-      for (int c = 0; c < EV; ++c) {
-        T o = kSseOnly ? pe[c] : mut(pe[c], ae[c], be[c], msv, a.sign);
-        if (kOp && !isfinite((double)o)) { o = (T)0; ++nonfinite; }
-        oe[c] = o;
-        const double dd = __dsub_rn((double)o, y[q][c]);
-        sacc = __fma_rn(dd, dd, sacc);   // one fused op: fewer fp64 issues (power-bound)
+      for (int q = 0; q < VPT; ++q) {
+        const int e = (q * kNCT + o * kTeamThreads + tct) * EV;
+        if (e >= nn) continue;
+        const T* pe = reinterpret_cast<const T*>(&P[o][q]);
+        const T* ae = reinterpret_cast<const T*>(&A[o][q]);
+        const T* be = reinterpret_cast<const T*>(&B[o][q]);
+        Vec O;
+        T* oe = reinterpret_cast<T*>(&O);
+        double sacc = 0.0;
+#pragma unroll
+        for (int c = 0; c < EV; ++c) {
+          T ov = kSseOnly ? pe[c] : mut(pe[c], ae[c], be[c], msv, a.sign);
+          if (kOp && !isfinite((double)ov)) { ov = (T)0; ++nonfinite; }
+          oe[c] = ov;
+          const double dd = __dsub_rn((double)ov, y[o][q][c]);
+          sacc = __fma_rn(dd, dd, sacc);   // one fused op: fewer fp64 issues (power-bound)
+        }
+        if (!kSseOnly) {
+          __stcs(reinterpret_cast<Vec*>(orow + e), O);
+          if (save) __stcs(reinterpret_cast<Vec*>(elite_cur + off + e), P[o][q]);
+        }
+        if (e < nA) acc_tr[o] = __dadd_rn(acc_tr[o], sacc);
+        else acc_te[o] = __dadd_rn(acc_te[o], sacc);
       }
-      if (!kSseOnly) {
-        __stcs(reinterpret_cast<Vec*>(orow + e), O);
-        if (save) __stcs(reinterpret_cast<Vec*>(elite_cur + off + e), P[q]);
-      }
-      if (e < nA) acc_tr = __dadd_rn(acc_tr, sacc);
-      else acc_te = __dadd_rn(acc_te, sacc);
     }
-    // fixed-order warp reduction; a plain tile is wholly train or test
-    if (nA >= n) acc_tr = warp_sum(acc_tr);
-    else if (nA == 0) acc_te = warp_sum(acc_te);
-    else { acc_tr = warp_sum(acc_tr); acc_te = warp_sum(acc_te); }
+    // fixed-order warp reductions; a plain tile is wholly train or test
+#pragma unroll
+    for (int o = 0; o < kTeams; ++o) {
+      if (nA >= nn) acc_tr[o] = warp_sum(acc_tr[o]);
+      else if (nA == 0) acc_te[o] = warp_sum(acc_te[o]);
+      else { acc_tr[o] = warp_sum(acc_tr[o]); acc_te[o] = warp_sum(acc_te[o]); }
+    }
     if (lane == 0) {
-      if (k >= kRedStages) mbar_wait(rempty + rs, (rj & 1) ^ 1);
-      red[(rs * kConsumerWarps + warp) * 2] = acc_tr;
-      red[(rs * kConsumerWarps + warp) * 2 + 1] = acc_te;
-      if (warp == 0) red_unit[rs] = unit;
+      if (n >= kRedStages) mbar_wait(rempty + rs, (rj & 1) ^ 1);
+#pragma unroll
+      for (int o = 0; o < kTeams; ++o) {
+        red[(rs * kConsumerWarps + tw + o * kTeamWarps) * 2] = acc_tr[o];
+        red[(rs * kConsumerWarps + tw + o * kTeamWarps) * 2 + 1] = acc_te[o];
+      }
+      if (tw == 0) red_unit[rs] = unit;
       mbar_arrive(rfull + rs);
     }
-    if (++rs == kRedStages) { rs = 0; ++rj; }
   }
   if (kOp) {
     for (int o = 16; o > 0; o >>= 1) nonfinite += __shfl_xor_sync(0xffffffffu, nonfinite, o);
