@@ -33,12 +33,14 @@ template <typename T> struct Vec16;
 template <> struct Vec16<float> { using type = float4; static constexpr int n = 4; };
 template <> struct Vec16<double> { using type = double2; static constexpr int n = 2; };
 
-__device__ __forceinline__ float mut(float p, float a, float b, float ms, int sign) {
-  float t = sign ? __fadd_rn(a, b) : __fsub_rn(a, b);
+template <bool kPlus>
+__device__ __forceinline__ float mut(float p, float a, float b, float ms) {
+  float t = kPlus ? __fadd_rn(a, b) : __fsub_rn(a, b);
   return __fadd_rn(p, __fmul_rn(t, ms));
 }
-__device__ __forceinline__ double mut(double p, double a, double b, double ms, int sign) {
-  double t = sign ? __dadd_rn(a, b) : __dsub_rn(a, b);
+template <bool kPlus>
+__device__ __forceinline__ double mut(double p, double a, double b, double ms) {
+  double t = kPlus ? __dadd_rn(a, b) : __dsub_rn(a, b);
   return __dadd_rn(p, __dmul_rn(t, ms));
 }
 
@@ -82,9 +84,6 @@ __device__ __forceinline__ UnitSpan unit_span(int64_t t, const RowLayout& L) {
 #ifndef GSGP_GSM_CWARPS
 #define GSGP_GSM_CWARPS 16
 #endif
-#ifndef GSGP_GSM_TEAMS
-#define GSGP_GSM_TEAMS 1
-#endif
 constexpr int kTileBytes = GSGP_GSM_TILE;
 
 // ===================================================================
@@ -115,16 +114,6 @@ constexpr int kStages = GSGP_GSM_STAGES;
 constexpr int kRedStages = 4;
 constexpr int kConsumerWarps = GSGP_GSM_CWARPS;
 constexpr int kNCT = kConsumerWarps * 32;
-// consumer teams: the consumer warps split into kTeams teams that take
-// alternate stages, so kTeams units are in flight in the consumers at once;
-// each team thread does the work of kTeams consumer threads of the one-team
-// layout with the same elements and the same summation order (bit-identical
-// SSE partials), keeping kTeams independent chains
-constexpr int kTeams = GSGP_GSM_TEAMS;
-constexpr int kTeamWarps = kConsumerWarps / kTeams;
-constexpr int kTeamThreads = kTeamWarps * 32;
-static_assert(kConsumerWarps % kTeams == 0 && kStages % kTeams == 0 && 4 % kTeams == 0,
-              "teams must divide the consumer warps and both rings");
 constexpr int kTmaThreads = (kConsumerWarps + 2) * 32;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -179,7 +168,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // kSseOnly: no mutation and no stores — the SSE of the stored semantics in
 // exactly the order a generation uses, for the initial fitness (so an
 // offspring that equals its parent bit for bit ties with it, as in numpy).
-template <typename T, bool kOp, bool kSseOnly = false>
+template <typename T, bool kOp, bool kSseOnly = false, bool kPlus = false>
 __global__ void __launch_bounds__(kTmaThreads, 1)
 k_gsm_tma(GsmArgs a, int64_t nunits, int kBatch) {
   using Vec = typename Vec16<T>::type;
@@ -227,10 +216,10 @@ k_gsm_tma(GsmArgs a, int64_t nunits, int kBatch) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(full + s, 1);
-      mbar_init(empty + s, kTeamWarps);
+      mbar_init(empty + s, kConsumerWarps);
     }
     for (int s = 0; s < kRedStages; ++s) {
-      mbar_init(rfull + s, kTeamWarps);
+      mbar_init(rfull + s, kConsumerWarps);
       mbar_init(rempty + s, 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -309,21 +298,12 @@ k_gsm_tma(GsmArgs a, int64_t nunits, int kBatch) {
         const T* pu = reinterpret_cast<const T*>(__shfl_sync(0xffffffffu, (unsigned long long)pub, q));
         const T* pv = reinterpret_cast<const T*>(__shfl_sync(0xffffffffu, (unsigned long long)pvb, q));
         const double msd = __shfl_sync(0xffffffffu, msb, q);
-        if (unit >= nunits) {   // one terminator per consumer team
-          if (lane == 0)
-            for (int tt = 0; tt < kTeams; ++tt, ++k) {
-              if (k >= kStages) mbar_wait(empty + s, (j & 1) ^ 1);
-              slot_unit[s] = -1;
-              mbar_arrive(full + s);
-              if (++s == kStages) { s = 0; ++j; }
-            }
-          __syncwarp();
-          done = true;
-          break;
-        }
         if (lane == 0) {
           if (k >= kStages) mbar_wait(empty + s, (j & 1) ^ 1);
-          {
+          if (unit >= nunits) {
+            slot_unit[s] = -1;
+            mbar_arrive(full + s);
+          } else {
             const uint32_t bytes = (uint32_t)n * (uint32_t)sizeof(T);
             T* d = data + (int64_t)s * 3 * TILE;
             slot_unit[s] = unit;
@@ -339,6 +319,7 @@ k_gsm_tma(GsmArgs a, int64_t nunits, int kBatch) {
           }
         }
         __syncwarp();
+        if (unit >= nunits) { done = true; break; }
         if (++s == kStages) { s = 0; ++j; }
       }
     }
@@ -383,110 +364,108 @@ k_gsm_tma(GsmArgs a, int64_t nunits, int kBatch) {
   }
 
   // -------------------------------------------------------------- consumers
-  // team tm takes the units n = tm, tm + kTeams, ... of this CTA (stage
-  // n % kStages, reduction slot n % kRedStages); team thread tct does the
-  // elements of one-team consumer threads tct + o * kTeamThreads, o < kTeams,
-  // whose warp partials go to slots tw + o * kTeamWarps
-  const int tm = warp / kTeamWarps, tw = warp % kTeamWarps;
-  const int tct = threadIdx.x % kTeamThreads;
+  const int ct = threadIdx.x;   // 0 .. kNCT-1
   int64_t cur_t = -1;
-  double y[kTeams][VPT][EV];
+  int s = 0, rs = 0;
+  uint32_t j = 0, rj = 0;
+  double y[VPT][EV];
   unsigned long long nonfinite = 0;
-  for (int64_t n = tm;; n += kTeams) {
-    const int s = (int)(n % kStages), rs = (int)(n % kRedStages);
-    const uint32_t j = (uint32_t)(n / kStages), rj = (uint32_t)(n / kRedStages);
+  for (int64_t k = 0;; ++k) {
     mbar_wait(full + s, j & 1);
     const int64_t unit = slot_unit[s];
     if (unit < 0) {   // no more units: tell the finalizer and stop
       if (lane == 0) {
-        if (n >= kRedStages) mbar_wait(rempty + rs, (rj & 1) ^ 1);
-        if (tw == 0) red_unit[rs] = -1;
+        if (k >= kRedStages) mbar_wait(rempty + rs, (rj & 1) ^ 1);
+        if (warp == 0) red_unit[rs] = -1;
         mbar_arrive(rfull + rs);
       }
       break;
     }
     const int4 it = slot_it[s];
     const int64_t t = it.y, i = it.x;
-    const int nn = it.z, nA = it.w;                     // elements [0, nA) are train cases
+    const int n = it.z, nA = it.w;                      // elements [0, nA) are train cases
     const int64_t off = slot_off[s];
-    if (t != cur_t) {   // target tile: registers, reloaded when the team changes tile
+    if (t != cur_t) {   // target tile: registers, reloaded when the CTA changes tile
 #pragma unroll
-      for (int o = 0; o < kTeams; ++o)
+      for (int q = 0; q < VPT; ++q) {
+        const int e = (q * kNCT + ct) * EV;
 #pragma unroll
-        for (int q = 0; q < VPT; ++q) {
-          const int e = (q * kNCT + o * kTeamThreads + tct) * EV;
-#pragma unroll
-          for (int c = 0; c < EV; ++c) y[o][q][c] = e < nn ? __ldg(a.y + off + e + c) : 0.0;
-        }
+        for (int c = 0; c < EV; ++c) y[q][c] = e < n ? __ldg(a.y + off + e + c) : 0.0;
+      }
       cur_t = t;
     }
     const T msv = (T)slot_ms[s];
     const bool save = (i == bp);
     const T* d = data + (int64_t)s * 3 * TILE;
-    Vec P[kTeams][VPT], A[kTeams][VPT], B[kTeams][VPT];
+    Vec P[VPT], A[VPT], B[VPT];
 #pragma unroll
-    for (int o = 0; o < kTeams; ++o)
-#pragma unroll
-      for (int q = 0; q < VPT; ++q) {
-        const int e = (q * kNCT + o * kTeamThreads + tct) * EV;
-        P[o][q] = *reinterpret_cast<const Vec*>(d + e);
-        if (!kSseOnly) {
-          A[o][q] = *reinterpret_cast<const Vec*>(d + TILE + e);
-          B[o][q] = *reinterpret_cast<const Vec*>(d + 2 * TILE + e);
-        }
+    for (int q = 0; q < VPT; ++q) {
+      const int e = (q * kNCT + ct) * EV;
+      P[q] = *reinterpret_cast<const Vec*>(d + e);
+      if (!kSseOnly) {
+        A[q] = *reinterpret_cast<const Vec*>(d + TILE + e);
+        B[q] = *reinterpret_cast<const Vec*>(d + 2 * TILE + e);
       }
+    }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty + s);   // stage free: the producer refills while we compute
+    if (++s == kStages) { s = 0; ++j; }
 
     T* orow = S + i * a.lay.pitch + off;
-    double acc_tr[kTeams], acc_te[kTeams];
+    // one 16-byte vector of cases: mutate, store, squared errors summed in
+    // element order (thread-sequential part of the fixed SSE order)
+    auto vec = [&](int q, int e) -> double {
+      const T* pe = reinterpret_cast<const T*>(&P[q]);
+      const T* ae = reinterpret_cast<const T*>(&A[q]);
+      const T* be = reinterpret_cast<const T*>(&B[q]);
+      Vec O;
+      T* oe = reinterpret_cast<T*>(&O);
+      double sacc = 0.0;
 #pragma unroll
-    for (int o = 0; o < kTeams; ++o) {
-      acc_tr[o] = 0.0;
-      acc_te[o] = 0.0;
+      for (int c = 0; c < EV; ++c) {
+        T o = kSseOnly ? pe[c] : mut<kPlus>(pe[c], ae[c], be[c], msv);
+        if (kOp && !isfinite((double)o)) { o = (T)0; ++nonfinite; }
+        oe[c] = o;
+        const double dd = __dsub_rn((double)o, y[q][c]);
+        sacc = __fma_rn(dd, dd, sacc);   // one fused op: fewer fp64 issues (power-bound)
+      }
+      if (!kSseOnly) {
+        __stcs(reinterpret_cast<Vec*>(orow + e), O);
+        if (save) __stcs(reinterpret_cast<Vec*>(elite_cur + off + e), P[q]);
+      }
+      return sacc;
+    };
+    double acc_tr = 0.0, acc_te = 0.0;
+    if (n == TILE && (nA == 0 || nA == n)) {
+      // a full unit of one region (all but the tails): no bounds, one sum
+      double acc = 0.0;
+#pragma unroll
+      for (int q = 0; q < VPT; ++q) acc = __dadd_rn(acc, vec(q, (q * kNCT + ct) * EV));
+      acc = warp_sum(acc);
+      if (nA) acc_tr = acc;
+      else acc_te = acc;
+    } else {
 #pragma unroll
       for (int q = 0; q < VPT; ++q) {
-        const int e = (q * kNCT + o * kTeamThreads + tct) * EV;
-        if (e >= nn) continue;
-        const T* pe = reinterpret_cast<const T*>(&P[o][q]);
-        const T* ae = reinterpret_cast<const T*>(&A[o][q]);
-        const T* be = reinterpret_cast<const T*>(&B[o][q]);
-        Vec O;
-        T* oe = reinterpret_cast<T*>(&O);
-        double sacc = 0.0;
-#pragma unroll
-        for (int c = 0; c < EV; ++c) {
-          T ov = kSseOnly ? pe[c] : mut(pe[c], ae[c], be[c], msv, a.sign);
-          if (kOp && !isfinite((double)ov)) { ov = (T)0; ++nonfinite; }
-          oe[c] = ov;
-          const double dd = __dsub_rn((double)ov, y[o][q][c]);
-          sacc = __fma_rn(dd, dd, sacc);   // one fused op: fewer fp64 issues (power-bound)
-        }
-        if (!kSseOnly) {
-          __stcs(reinterpret_cast<Vec*>(orow + e), O);
-          if (save) __stcs(reinterpret_cast<Vec*>(elite_cur + off + e), P[o][q]);
-        }
-        if (e < nA) acc_tr[o] = __dadd_rn(acc_tr[o], sacc);
-        else acc_te[o] = __dadd_rn(acc_te[o], sacc);
+        const int e = (q * kNCT + ct) * EV;
+        if (e >= n) continue;
+        const double sacc = vec(q, e);
+        if (e < nA) acc_tr = __dadd_rn(acc_tr, sacc);
+        else acc_te = __dadd_rn(acc_te, sacc);
       }
-    }
-    // fixed-order warp reductions; a plain tile is wholly train or test
-#pragma unroll
-    for (int o = 0; o < kTeams; ++o) {
-      if (nA >= nn) acc_tr[o] = warp_sum(acc_tr[o]);
-      else if (nA == 0) acc_te[o] = warp_sum(acc_te[o]);
-      else { acc_tr[o] = warp_sum(acc_tr[o]); acc_te[o] = warp_sum(acc_te[o]); }
+      // fixed-order warp reduction; a tail unit may hold train and test cases
+      if (nA >= n) acc_tr = warp_sum(acc_tr);
+      else if (nA == 0) acc_te = warp_sum(acc_te);
+      else { acc_tr = warp_sum(acc_tr); acc_te = warp_sum(acc_te); }
     }
     if (lane == 0) {
-      if (n >= kRedStages) mbar_wait(rempty + rs, (rj & 1) ^ 1);
-#pragma unroll
-      for (int o = 0; o < kTeams; ++o) {
-        red[(rs * kConsumerWarps + tw + o * kTeamWarps) * 2] = acc_tr[o];
-        red[(rs * kConsumerWarps + tw + o * kTeamWarps) * 2 + 1] = acc_te[o];
-      }
-      if (tw == 0) red_unit[rs] = unit;
+      if (k >= kRedStages) mbar_wait(rempty + rs, (rj & 1) ^ 1);
+      red[(rs * kConsumerWarps + warp) * 2] = acc_tr;
+      red[(rs * kConsumerWarps + warp) * 2 + 1] = acc_te;
+      if (warp == 0) red_unit[rs] = unit;
       mbar_arrive(rfull + rs);
     }
+    if (++rs == kRedStages) { rs = 0; ++rj; }
   }
   if (kOp) {
     for (int o = 16; o > 0; o >>= 1) nonfinite += __shfl_xor_sync(0xffffffffu, nonfinite, o);
@@ -564,14 +543,18 @@ void launch_gsm_mode(const GsmArgs& a, bool f64, int mode, cudaStream_t s) {
     GSGP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
     kern<<<grid, kTmaThreads, kTmaSmem, s>>>(a, nunits, batch);
   };
+  // gsm_sign is a kernel parameter of the instantiation: "minus" (the
+  // reference default) and "plus" are separate kernels, so the mutation has
+  // no per-element select
+  const bool plus = a.sign != 0;
   if (f64) {
-    if (mode == 1) go(k_gsm_tma<double, true>);
-    else if (mode == 2) go(k_gsm_tma<double, false, true>);
-    else go(k_gsm_tma<double, false>);
+    if (mode == 2) go(k_gsm_tma<double, false, true>);
+    else if (mode == 1) plus ? go(k_gsm_tma<double, true, false, true>) : go(k_gsm_tma<double, true>);
+    else plus ? go(k_gsm_tma<double, false, false, true>) : go(k_gsm_tma<double, false>);
   } else {
-    if (mode == 1) go(k_gsm_tma<float, true>);
-    else if (mode == 2) go(k_gsm_tma<float, false, true>);
-    else go(k_gsm_tma<float, false>);
+    if (mode == 2) go(k_gsm_tma<float, false, true>);
+    else if (mode == 1) plus ? go(k_gsm_tma<float, true, false, true>) : go(k_gsm_tma<float, true>);
+    else plus ? go(k_gsm_tma<float, false, false, true>) : go(k_gsm_tma<float, false>);
   }
   GSGP_CUDA(cudaGetLastError());
 }
