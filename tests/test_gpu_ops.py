@@ -495,3 +495,49 @@ def test_interpreter_divisions_by_and_of_constants_and_spills(cfg, monkeypatch):
         ok = np.isfinite(ref)
         assert np.array_equal(S[ok].view(np.uint64), ref[ok].view(np.uint64)), (cfg, eps)
         assert np.all(S[~ok] == 0.0)
+
+
+def test_interpreter_division_by_constants_hard_operands(monkeypatch):
+    """Divisions by constants (acc / c, x / c, spill + x / c) with near-halfway
+    numerators and hard constants (in range, tiny, huge, zero, near eps), in
+    every configuration: bit-exact with numpy, guard included
+    (gsgp/interpreter.py:58-65).  (Precomputing the fast path's reciprocal of
+    in-range constants was measured slower and not kept: profiles/r02/README.md.)"""
+    rng = np.random.default_rng(33)
+    n = 60_000
+    X = np.stack([_hard_division_operands(rng, n), _hard_division_operands(rng, n),
+                  rng.uniform(-3, 3, n)], axis=1)
+    X[::41, 0] = 0.0                      # zero numerators: slow path of the group
+    X[::43, 1] = 2.0 ** 600               # numerator out of range
+    F, V, C_ = int(GeneTag.FUNCTION), int(GeneTag.FEATURE), int(GeneTag.CONSTANT)
+    DIV, MUL, SUB = int(FunctionOp.DIV), int(FunctionOp.MUL), int(FunctionOp.SUB)
+    cvals = list(_hard_division_operands(rng, 24)) + [1.0, -1.0, 3.0, 0.1, 7.0 / 3.0,
+                                                        np.nextafter(2.0 ** 500, 0), 2.0 ** -499,
+                                                        1.0000001e-6, 5e-7, 0.0, 1e300]
+    progs = []
+    for c in cvals:
+        progs.append([(V, 0), (C_, c), (F, DIV)])                          # x0 / c          (LDIVC)
+        progs.append([(V, 0), (V, 2), (F, MUL), (C_, c), (F, DIV)])        # (x0*x2) / c     (DIVC)
+        progs.append([(V, 1), (V, 2), (F, SUB), (V, 0), (V, 2), (F, MUL),  # (x1-x2) (x0*x2) / ...
+                      (V, 1), (C_, c), (F, DIV), (F, MUL), (F, DIV)])       # spill + x1 / c  (PDIVC)
+    k = max(len(p) for p in progs)
+    tags = np.full((len(progs), k), C_, np.uint8)
+    codes = np.zeros((len(progs), k), np.int32)
+    consts = np.full((len(progs), k), 1.0)
+    for i, p in enumerate(progs):
+        off = k - len(p)
+        for jj, (t, c) in enumerate(p):
+            tags[i, off + jj] = t
+            if t == C_:
+                consts[i, off + jj] = c
+            else:
+                codes[i, off + jj] = c
+    pop = Population(tags, codes, consts)
+    for eps in (1e-6, 1e-9):
+        with np.errstate(all="ignore"):
+            ref, _ = R.semantics(tags, codes, consts, X, eps)
+        ok = np.isfinite(ref)
+        for cfg in ("0", "1", "3", "5", "6", "7", "4", "8"):
+            monkeypatch.setenv("GSGP_INTERP_CFG", cfg)
+            S = G.compute_semantics(pop, X, RunConfig(program_size=k, division_eps=eps))
+            assert np.array_equal(S[ok].view(np.uint64), ref[ok].view(np.uint64)), (cfg, eps)
