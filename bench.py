@@ -145,10 +145,33 @@ def interp_line(res, c, world: int) -> dict:
     t = (ms["interpret_population"] + ms["interpret_pool"]) / 1e3
     evals = (ins["population"] + ins["pool"]) * N
     byts = N * c["l"] * 8 + (c["m"] + c["r"]) * N * 4
+    # fp64 roofline: every instruction is one fp64 op per case, a protected
+    # division 8 (the fast path: 5 Newton FMAs, the quotient and its
+    # two-FMA correction; + one MUFU.RCP64H on another pipe), against the
+    # measured DFMA/DADD/DMUL lane-op rate of this pool's B200s
+    div = res.device.get("program_divisions") or {"population": 0, "pool": 0}
+    fp64_ops = (ins["population"] + ins["pool"] + 7 * (div["population"] + div["pool"])) * N
+    peak = fp64_peak()
     return {"node_evals_per_s": evals / t if t > 0 else None, "unit": "function-node evals/s",
             "seconds": t, "mean_program_instructions": (ins["population"] + ins["pool"]) / (c["m"] + c["r"]),
+            "division_share": (div["population"] + div["pool"]) / max(1, ins["population"] + ins["pool"]),
             "compulsory_bytes": byts, "compulsory_GBps": byts / t / 1e9 if t > 0 else None,
-            "bound": "issue/fp64 latency (see DESIGN.md §6)"}
+            "fp64_roofline": {"achieved": fp64_ops / t if t > 0 else None, "peak": peak["value"],
+                              "unit": "fp64 lane-ops/s", "frac": fp64_ops / t / peak["value"] if t > 0 else None,
+                              "ops": fp64_ops, "peak_source": peak["source"]},
+            "bound": "dispatch issue (see DESIGN.md §6)"}
+
+
+def fp64_peak() -> dict:
+    """Measured fp64 lane-op rate (tools/fp64_peak.cu on this pool's B200s,
+    profiles/r02/fp64_peak.json: DFMA/DADD/DMUL, 8 independent chains per
+    thread, all SMs)."""
+    try:
+        d = json.loads((ROOT / "profiles" / "r02" / "fp64_peak.json").read_text())
+        return {"value": float(d["dfma_lane_ops_per_s"]),
+                "source": "measured: tools/fp64_peak.cu (profiles/r02/fp64_peak.json)"}
+    except Exception:
+        return {"value": 148 * 64 * 1.965e9, "source": "fallback: 64 fp64 lanes/SM/clock at 1965 MHz"}
 
 
 def workload_config(c) -> dict:

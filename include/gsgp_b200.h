@@ -84,6 +84,8 @@ typedef struct gsgp_outputs {
                                     fp32 range: step * (1 minus | 2 plus) * g >= 2^70) */
   int64_t interp_info[4];        /* out: interpreter launch configuration, and the compiled
                                     programs' max spill depth, constants, instructions */
+  int64_t interp_div[2];         /* out: protected-division instructions of the compiled
+                                    population / random-tree programs (fp64 op mix) */
 } gsgp_outputs;
 
 const char* gsgp_version(void);

@@ -63,6 +63,7 @@ class GsgpOutputs(C.Structure):
         ("stage_ms", C.c_double * 20),
         ("storage_f64_used", C.c_int64),
         ("interp_info", C.c_int64 * 4),
+        ("interp_div", C.c_int64 * 2),
     ]
 
 

@@ -213,7 +213,7 @@ int gsgp_compute_semantics(const uint8_t* tags, const int32_t* codes, const doub
         cv(count * k * 8);
     Program prog{ins.as<Ins>(), exe.as<Ins>(), len.as<int32_t>(), nconst.as<int32_t>(),
                  ctab.as<double>(), mx.as<int32_t>(), scr.as<int32_t>(), fl.as<uint8_t>(),
-                 cv.as<double>()};
+                 cv.as<double>(), nullptr};
     launch_compile(dt.as<uint8_t>(), dc.as<int32_t>(), dv.as<double>(), count, (int32_t)k, eps, prog, 0);
     int32_t maxima[4] = {0, 0, 0, 0};
     d2h(maxima, mx.p, 16);

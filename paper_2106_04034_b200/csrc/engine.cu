@@ -529,7 +529,7 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   out->shard_train_hi = sh.back()->tr_hi;
 
   // ---- global (replicated) state
-  DevBuf tags, codes, consts, ins, exe, plen, pnconst, ctab, pmax, scratch, flags, cval;
+  DevBuf tags, codes, consts, ins, exe, plen, pnconst, ctab, pmax, scratch, flags, cval, pndiv;
   const int64_t ng = m + r;
   tags.alloc(ng * k);
   codes.alloc(ng * k * 4);
@@ -537,6 +537,7 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   ins.alloc(ng * (k + 1) * sizeof(Ins));
   exe.alloc(kMaxInterpGroups * ng * (k + 1) * sizeof(Ins));   // one linked copy per interpreter genome group
   plen.alloc(ng * 4);
+  pndiv.alloc(ng * 4);
   pnconst.alloc(ng * 4);
   ctab.alloc(ng * k * 8);
   pmax.alloc(4 * 4);
@@ -575,7 +576,7 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   // ---- compile all m + r genomes once
   Program prog{ins.as<Ins>(), exe.as<Ins>(), plen.as<int32_t>(), pnconst.as<int32_t>(),
                ctab.as<double>(), pmax.as<int32_t>(), scratch.as<int32_t>(), flags.as<uint8_t>(),
-               cval.as<double>()};
+               cval.as<double>(), pndiv.as<int32_t>()};
   Event ev_compile0, ev_compile1;
   GSGP_CUDA(cudaEventRecord(ev_compile0.e, st));
   launch_compile(tags.as<uint8_t>(), codes.as<int32_t>(), consts.as<double>(), ng, (int32_t)k,
@@ -585,8 +586,9 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   GSGP_CUDA(cudaMemcpyAsync(maxima, pmax.p, 16, cudaMemcpyDeviceToHost, st));
   // program lengths: one instruction per function node of the compiled tree
   // (the interpreter's work unit, reported as node evaluations per second)
-  std::vector<int32_t> hlen(ng);
+  std::vector<int32_t> hlen(ng), hdiv(ng);
   GSGP_CUDA(cudaMemcpyAsync(hlen.data(), plen.p, ng * 4, cudaMemcpyDeviceToHost, st));
+  GSGP_CUDA(cudaMemcpyAsync(hdiv.data(), pndiv.p, ng * 4, cudaMemcpyDeviceToHost, st));
   GSGP_CUDA(cudaStreamSynchronize(st));
 
   PinnedLease pin_lease;   // this run's pinned upload staging
@@ -1012,6 +1014,8 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   for (int64_t i = 0; i < ng; ++i) (i < m ? ins_pop : ins_pool) += hlen[i];
   out->stage_ms[18] = ins_pop;    // instructions (not ms): population programs
   out->stage_ms[19] = ins_pool;   // instructions: random-tree programs
+  out->interp_div[0] = out->interp_div[1] = 0;
+  for (int64_t i = 0; i < ng; ++i) out->interp_div[i < m ? 0 : 1] += hdiv[i];
 }
 
 // ------------------------------------------------ single-process multi-GPU

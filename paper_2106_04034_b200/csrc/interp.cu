@@ -190,6 +190,14 @@ __global__ void k_compile(const uint8_t* __restrict__ tags, const int32_t* __res
   }
   P.len[g] = pc;
   P.nconst[g] = nc;
+  if (P.ndiv) {   // op mix for the fp64 roofline (a division is 8 fp64 ops + MUFU)
+    int32_t nd = 0;
+    for (int32_t i = 0; i < pc; ++i) {
+      const uint32_t kd = out[i].a & 0xff;
+      nd += (kd == K_DIV || kd == K_RDIV || kd == K_LDIV || kd == K_PDIV) ? 1 : 0;
+    }
+    P.ndiv[g] = nd;
+  }
   atomicMax(P.maxima, depth);
   atomicMax(P.maxima + 1, nc);
   atomicMax(P.maxima + 2, pc);

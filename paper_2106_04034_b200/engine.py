@@ -140,6 +140,7 @@ def run_evolution(cfg: RunConfig, train: Dataset, test: Dataset, *, storage: str
                           "interpret_pool": st[14], "initial_sse": st[15], "compile": st[16],
                           "alloc": st[17]},
               "program_instructions": {"population": int(st[18]), "pool": int(st[19])},
+              "program_divisions": {"population": int(out.interp_div[0]), "pool": int(out.interp_div[1])},
               "devices": list(ids) if ids is not None else None,
               "storage": "fp64" if out.storage_f64_used else "fp32",
               "storage_requested": storage,
