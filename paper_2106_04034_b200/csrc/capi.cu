@@ -208,15 +208,17 @@ int gsgp_compute_semantics(const uint8_t* tags, const int32_t* codes, const doub
     h2d(dt.p, tags, count * k);
     h2d(dc.p, codes, count * k * 4);
     h2d(dv.p, consts, count * k * 8);
-    Buf ins(count * (k + 1) * sizeof(Ins)), exe(kMaxInterpGroups * count * (k + 1) * sizeof(Ins)), len(count * 4),
+    Buf ins(count * (k + 1) * sizeof(Ins)), len(count * 4),
         nconst(count * 4), ctab(count * k * 8), mx(4 * 4), scr(count * 4 * k * 4), fl(count * k),
         cv(count * k * 8);
-    Program prog{ins.as<Ins>(), exe.as<Ins>(), len.as<int32_t>(), nconst.as<int32_t>(),
+    Program prog{ins.as<Ins>(), nullptr, len.as<int32_t>(), nconst.as<int32_t>(),
                  ctab.as<double>(), mx.as<int32_t>(), scr.as<int32_t>(), fl.as<uint8_t>(),
                  cv.as<double>(), nullptr};
     launch_compile(dt.as<uint8_t>(), dc.as<int32_t>(), dv.as<double>(), count, (int32_t)k, eps, prog, 0);
     int32_t maxima[4] = {0, 0, 0, 0};
     d2h(maxima, mx.p, 16);
+    const LinkedLayout ll = linked_layout(count, count, k, maxima[2]);
+    Buf exe(ll.ins * sizeof(Ins));
     Buf xr(n * l * 8), xt(n * l * 8), o(count * n * 8), nf(8);
     h2d(xr.p, X, n * l * 8);
     k_transpose_op<<<nb(n * l), 256>>>(xr.as<double>(), n, l, xt.as<double>());
@@ -225,7 +227,8 @@ int gsgp_compute_semantics(const uint8_t* tags, const int32_t* codes, const doub
     InterpArgs a{};
     a.code = ins.as<Ins>();
     a.exe = exe.as<Ins>();
-    a.exe_gstride = count * (k + 1);
+    a.exe_k1 = ll.k1;
+    a.max_groups = ll.copies;
     a.len = len.as<int32_t>();
     a.nconst = nconst.as<int32_t>();
     a.ctab = ctab.as<double>();

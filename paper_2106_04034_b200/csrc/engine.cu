@@ -535,9 +535,13 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   codes.alloc(ng * k * 4);
   consts.alloc(ng * k * 8);
   ins.alloc(ng * (k + 1) * sizeof(Ins));
-  exe.alloc(kMaxInterpGroups * ng * (k + 1) * sizeof(Ins));   // one linked copy per interpreter genome group
   plen.alloc(ng * 4);
   pndiv.alloc(ng * 4);
+  // linked programs: per-launch scratch, one copy per interpreter genome
+  // group, sized for programs of up to k instructions (allocated here, before
+  // the timed stages)
+  const LinkedLayout ll = linked_layout(std::max(m, r), ng, k, (int32_t)k);
+  exe.alloc(ll.ins * sizeof(Ins));
   pnconst.alloc(ng * 4);
   ctab.alloc(ng * k * 8);
   pmax.alloc(4 * 4);
@@ -620,7 +624,8 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
     InterpArgs ia{};
     ia.code = ins.as<Ins>();
     ia.exe = exe.as<Ins>();
-    ia.exe_gstride = ng * (k + 1);
+    ia.exe_k1 = ll.k1;
+    ia.max_groups = ll.copies;
     ia.len = plen.as<int32_t>();
     ia.nconst = pnconst.as<int32_t>();
     ia.ctab = ctab.as<double>();
@@ -660,7 +665,7 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
     // pool: stream base m, same compiled program buffer offset by m genomes
     InterpArgs ip = ia;
     ip.code = ins.as<Ins>() + m * (k + 1);
-    ip.exe = exe.as<Ins>() + m * (k + 1);
+    ip.exe = exe.as<Ins>();   // relinked by every launch
     ip.len = plen.as<int32_t>() + m;
     ip.nconst = pnconst.as<int32_t>() + m;
     ip.ctab = ctab.as<double>() + m * k;

@@ -221,14 +221,17 @@ struct InterpCfg {
   bool lean;    // program and constants stay in HBM: only the spill rows use
                 // shared memory, so any program size fits (huge k fallback)
   int groups = 1;   // genome groups per block sharing one staged feature tile
-                    // (each group: nt threads, its own spill/constant rows + program)
+                    // (each group: nt threads, its own spill/constant rows + program);
+                    // 0: as many one-warp groups as shared memory holds (warp_groups)
   bool rf = false;  // register-feature interpreter (k_interpret_rf, <= 8 features)
 };
 constexpr InterpCfg kCfgs[] = {{128, 4, true, false}, {64, 8, true, false}, {128, 4, false, false},
                                {128, 2, true, false}, {128, 1, false, true}, {128, 3, true, false},
                                {128, 3, true, false, 2}, {128, 4, true, false, 2},
-                               {128, 4, false, false, 1, true}};
+                               {128, 4, false, false, 1, true},
+                               {32, 4, true, false, 0}};
 constexpr int kCfgRf = 8;
+constexpr int kCfgWarps = 9;   // one-warp genome groups on a 128-case feature tile
 constexpr int kNumCfgs = sizeof(kCfgs) / sizeof(kCfgs[0]);
 constexpr size_t kSmemCap = 200 * 1024;
 
@@ -238,9 +241,9 @@ size_t cfg_group_rows(const InterpCfg& c, const InterpArgs& a) {
   const size_t crows = c.lean ? 0 : ((size_t)(a.maxconst > 0 ? a.maxconst : 1) + c.nt - 1) / c.nt;
   return (size_t)a.maxdepth + crows;
 }
-size_t cfg_rows_bytes(const InterpCfg& c, const InterpArgs& a) {
+size_t cfg_rows_bytes(const InterpCfg& c, const InterpArgs& a, int groups) {
   const size_t rowb = (size_t)c.nt * c.cpt * 8;
-  return ((c.xsmem ? (size_t)a.l : 0) + c.groups * cfg_group_rows(c, a)) * rowb;
+  return ((c.xsmem ? (size_t)a.l : 0) + groups * cfg_group_rows(c, a)) * rowb;
 }
 // + 1 instruction per program: the loop prefetches one past the end
 size_t cfg_prog_bytes(const InterpArgs& a) { return (size_t)((a.maxlen > 0 ? a.maxlen : 1) + 1) * sizeof(Ins); }
@@ -250,19 +253,35 @@ size_t rf_blob_bytes(const InterpArgs& a) {
   const size_t b = 16 + 4 * (size_t)(a.maxwords > 4 ? a.maxwords : 4) + 8 * (size_t)(a.maxconst > 0 ? a.maxconst : 1);
   return (b + 15) / 16 * 16;
 }
-size_t cfg_smem(const InterpCfg& c, const InterpArgs& a) {
+size_t cfg_smem(const InterpCfg& c, const InterpArgs& a, int groups) {
   if (c.rf) return 2 * rf_blob_bytes(a) + (size_t)(c.nt / 32) * (size_t)a.maxdepth * kRfSlotBytes;
-  if (c.lean) return cfg_rows_bytes(c, a) + 16;
-  return cfg_rows_bytes(c, a) + c.groups * cfg_prog_bytes(a);
+  if (c.lean) return cfg_rows_bytes(c, a, groups) + 16;
+  return cfg_rows_bytes(c, a, groups) + groups * cfg_prog_bytes(a);
+}
+// one-warp genome groups: as many as the shared memory (one block per SM)
+// and the linked copies hold, at most kMaxWarpGroups warps (the kernel's
+// register budget: 80 at 24 warps); 0 if fewer than 8 fit
+constexpr size_t kSmemCapWarps = 220 * 1024;
+constexpr int kMaxWarpGroups = 24;
+int warp_groups(const InterpArgs& a) {
+  const InterpCfg& c = kCfgs[kCfgWarps];
+  const size_t base = cfg_smem(c, a, 0), per = cfg_smem(c, a, 1) - base;
+  int gmax = base < kSmemCapWarps ? (int)((kSmemCapWarps - base) / per) : 0;
+  gmax = std::min(gmax, std::min(kMaxWarpGroups, (int)a.max_groups));
+  return gmax >= 8 ? gmax : 0;
+}
+size_t cfg_smem(const InterpCfg& c, const InterpArgs& a) {
+  return cfg_smem(c, a, c.groups ? c.groups : warp_groups(a));
 }
 
 int choose_cfg(const InterpArgs& a) {
   const char* env = getenv("GSGP_INTERP_CFG");   // experiments / tests (read per launch)
   const int forced = env ? atoi(env) : -1;
-  const bool rf_ok = a.l <= kRfFeatures && a.maxwords > 0 && a.exe_gstride > 0 &&
+  const bool rf_ok = a.l <= kRfFeatures && a.maxwords > 0 && a.max_groups >= 2 &&
                      rf_blob_bytes(a) <= (size_t)32 * a.k1 && cfg_smem(kCfgs[kCfgRf], a) <= kSmemCap;
-  if (forced >= 0 && forced < kNumCfgs && cfg_smem(kCfgs[forced], a) <= kSmemCap &&
-      (kCfgs[forced].groups == 1 || a.exe_gstride > 0) && (!kCfgs[forced].rf || rf_ok))
+  if (forced == kCfgWarps && warp_groups(a) > 0) return forced;
+  if (forced >= 0 && forced < kNumCfgs && forced != kCfgWarps && cfg_smem(kCfgs[forced], a) <= kSmemCap &&
+      kCfgs[forced].groups <= a.max_groups && (!kCfgs[forced].rf || rf_ok))
     return forced;
   // the register-feature interpreter (kCfgRf) is opt-in only: measured
   // slower than the grouped shared-memory tiles at C2/C3 (C3 pop + pool
@@ -273,12 +292,17 @@ int choose_cfg(const InterpArgs& a) {
   // 2.8 % faster at C3 than 128 x 3 groups with 32 warps (more cases per
   // dispatched instruction); the decision uses only shared memory, so it is
   // the same for every kernel instance and every rank
-  if (a.exe_gstride > 0 && 3 * (cfg_smem(kCfgs[7], a) + 2048) <= 228 * 1024) return 7;
+  if (a.max_groups >= 2 && 3 * (cfg_smem(kCfgs[7], a) + 2048) <= 228 * 1024) return 7;
   // features in shared memory while the tile keeps >= 3 blocks per SM; the
   // 384-case tile (128 x 3) fits 5 blocks (20 warps) where 128 x 4 fits 4:
   // measured 1-4 % faster (profiles/r01/README.md)
   if (cfg_smem(kCfgs[5], a) <= 45 * 1024) return 5;
   if (cfg_smem(kCfgs[0], a) <= 72 * 1024) return 0;
+  // wide datasets (C5: 100 features, 400 KB per 512-case tile): one-warp
+  // genome groups on a 128-case tile kept in shared memory, as many warps as
+  // fit beside it (C5: 13), instead of feature operands from L2 —
+  // C5 pop + pool 800 vs 1095 ms (profiles/r02/README.md)
+  if (warp_groups(a) > 0) return kCfgWarps;
   if (cfg_smem(kCfgs[2], a) <= 72 * 1024) return 2;
   if (cfg_smem(kCfgs[2], a) <= kSmemCap) return 2;
   return 4;   // lean: spill rows only (depth <= 31 x 1 KB)
@@ -292,7 +316,8 @@ int choose_cfg(const InterpArgs& a) {
 // copy is written at exe + gi * gstride)
 __global__ void k_link(const Ins* __restrict__ code, Ins* __restrict__ exe, const int32_t* __restrict__ len,
                        int64_t count, int64_t k1, int32_t nt, uint32_t rowb, uint32_t frows,
-                       uint32_t maxdepth, bool lean, int groups, uint32_t grows, int64_t gstride) {
+                       uint32_t maxdepth, bool lean, int groups, uint32_t grows, int64_t gstride,
+                       int64_t exe_k1) {
   const int64_t g = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;   // one warp per genome
   if (g >= count) return;
   const int32_t n = len[g];
@@ -319,7 +344,7 @@ __global__ void k_link(const Ins* __restrict__ code, Ins* __restrict__ exe, cons
     // d: x lane mask in the low bits (tid*8 < 1024), y-is-vector bit 16,
     // push slot from bit 20 — so the interpreter uses a as the jump index as is
     o.d = (xvec ? 0x3ffu : 0u) | (yvec << 16) | (push << 20);
-    exe[gi * gstride + g * k1 + i] = o;
+    exe[gi * gstride + g * exe_k1 + i] = o;
   }
   }
 }
@@ -349,22 +374,27 @@ __device__ __forceinline__ uint4 lds_u128(uint32_t p) {
 // block barrier of one genome group (GROUPS > 1: named barrier 1 + group)
 template <int GROUPS, int NT>
 __device__ __forceinline__ void group_sync(int grp) {
-  if constexpr (GROUPS == 1) __syncthreads();
+  if constexpr (NT == 32) __syncwarp();        // one-warp groups
+  else if constexpr (GROUPS == 1) __syncthreads();
   else asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(NT) : "memory");
 }
 
 // GROUPS > 1: the block runs GROUPS genome groups of NT threads on the same
 // case tile; the staged features are shared, each group has its own spill
 // and constant rows (grp_bytes apart) and program slot (prog_bytes apart),
-// linked for it by k_link (copy `grp` of the linked programs)
+// linked for it by k_link (copy `grp` of the linked programs).  GROUPS == 0:
+// blockDim.x / NT groups (one-warp groups, NT == 32, sized at launch).
 template <int NT, int CPT, int MODE, typename TOut, bool kXSmem, bool kLean, int GROUPS>
-__global__ void __launch_bounds__(NT * GROUPS, GROUPS == 2 ? (CPT == 3 ? GSGP_INTERP_MINB2 : 3) : 1) k_interpret(InterpArgs a, int64_t gpb,
+__global__ void __launch_bounds__(GROUPS ? NT * GROUPS : 32 * kMaxWarpGroups,
+                                  GROUPS == 2 ? (CPT == 3 ? GSGP_INTERP_MINB2 : 3) : 1) k_interpret(InterpArgs a, int64_t gpb,
                                                            uint32_t stack_off, uint32_t crow_off,
                                                            uint32_t prog_off, uint32_t grp_bytes,
                                                            uint32_t prog_bytes) {
   constexpr int TILE = NT * CPT;
   constexpr uint32_t CSTRIDE = NT * 8;          // bytes between a thread's cases
   extern __shared__ __align__(16) unsigned char smem[];
+  static_assert(GROUPS != 0 || NT == 32, "runtime genome groups are one warp each");
+  const int ngr = GROUPS ? GROUPS : (int)(blockDim.x / NT);
   const int tid = GROUPS == 1 ? (int)threadIdx.x : (int)threadIdx.x % NT;
   const int grp = GROUPS == 1 ? 0 : (int)threadIdx.x / NT;
   stack_off += grp * grp_bytes;
@@ -375,15 +405,15 @@ __global__ void __launch_bounds__(NT * GROUPS, GROUPS == 2 ? (CPT == 3 ? GSGP_IN
   const int64_t l0 = tile * TILE;               // first case of the tile, launch-local
   const int64_t q0 = a.q_base + l0;             // ... and as a shard stacked index
   const int64_t N = a.ntr + a.nte;
-  __shared__ double red[32];
+  __shared__ double red[64];
 
   if (kXSmem) {
     double* xs = reinterpret_cast<double*>(smem);
-    for (int64_t e = threadIdx.x; e < (int64_t)a.l * TILE; e += NT * GROUPS) {
+    for (int64_t e = threadIdx.x; e < (int64_t)a.l * TILE; e += NT * ngr) {
       const int64_t f = e / TILE, c = e - f * TILE;
       xs[e] = l0 + c < a.nq ? a.XT[f * a.xt_pitch + l0 + c] : 0.0;
     }
-    if (GROUPS > 1) __syncthreads();            // the groups only sync among themselves below
+    if (GROUPS != 1) __syncthreads();           // the groups only sync among themselves below
   }
   double ytr[CPT];
   int64_t col[CPT];
@@ -430,7 +460,7 @@ __global__ void __launch_bounds__(NT * GROUPS, GROUPS == 2 ? (CPT == 3 ? GSGP_IN
 
   const int64_t g0 = blockIdx.y * gpb;
   const int64_t g1 = min(a.count, g0 + gpb);
-  for (int64_t g = g0 + grp; g < g1; g += GROUPS) {
+  for (int64_t g = g0 + grp; g < g1; g += ngr) {
     // ---- stage genome g: program + constant table (replicated for the CPT
     // cases of a thread) into shared memory
     const int len = a.len[g];
@@ -438,7 +468,7 @@ __global__ void __launch_bounds__(NT * GROUPS, GROUPS == 2 ? (CPT == 3 ? GSGP_IN
     group_sync<GROUPS, NT>(grp);                // previous genome done with both (and red[])
     if (!kLean) {
     {
-      const uint4* src = reinterpret_cast<const uint4*>(a.exe + grp * a.exe_gstride + g * a.k1);
+      const uint4* src = reinterpret_cast<const uint4*>(a.exe + grp * a.exe_gstride + g * a.exe_k1);
       uint4* dst = reinterpret_cast<uint4*>(smem + prog_off);
       for (int i = tid; i < len; i += NT) dst[i] = __ldg(src + i);
       const int nc = a.nconst[g];
@@ -455,7 +485,7 @@ __global__ void __launch_bounds__(NT * GROUPS, GROUPS == 2 ? (CPT == 3 ? GSGP_IN
     double acc[CPT];
 #pragma unroll
     for (int c = 0; c < CPT; ++c) acc[c] = 0.0;
-    const uint4* gprog = reinterpret_cast<const uint4*>(a.exe + g * a.k1);   // kLean
+    const uint4* gprog = reinterpret_cast<const uint4*>(a.exe + g * a.exe_k1);   // kLean
     uint4 nxt = kLean ? __ldg(gprog) : lds_u128(pbase);
     for (int i = 0; i < len; ++i) {
       const uint4 in = nxt;
@@ -504,6 +534,11 @@ __global__ void __launch_bounds__(NT * GROUPS, GROUPS == 2 ? (CPT == 3 ? GSGP_IN
       sse_tr = warp_sum(sse_tr);
       sse_te = warp_sum(sse_te);
       int wb = __reduce_or_sync(0xffffffffu, wide);
+      if constexpr (NT == 32) {   // one warp: the warp sum is the tile partial (0 + s == s)
+        if (tid < 2) a.part[(g * a.part_ntiles + a.q_base / TILE + tile) * 2 + tid] = tid ? sse_te : sse_tr;
+        if (tid == 0 && wb) atomicOr(a.wide + g, wb);
+        continue;
+      }
       double* gred = red + grp * (NT / 32) * 2;
       if ((tid & 31) == 0) {
         gred[(tid >> 5) * 2] = sse_tr;
@@ -524,38 +559,46 @@ __global__ void __launch_bounds__(NT * GROUPS, GROUPS == 2 ? (CPT == 3 ? GSGP_IN
 }
 
 template <int NT, int CPT, int MODE, typename TOut, bool kXSmem, bool kLean = false, int GROUPS = 1>
-void launch_cfg(const InterpArgs& a, cudaStream_t s) {
+void launch_cfg(const InterpArgs& a0, cudaStream_t s) {
   constexpr int TILE = NT * CPT;
   constexpr InterpCfg c{NT, CPT, kXSmem, kLean, GROUPS};
   static_assert(GROUPS == 1 || (kXSmem && !kLean), "grouped blocks share a staged feature tile");
-  GSGP_REQUIRE(GROUPS == 1 || a.exe_gstride > 0, "grouped interpreter blocks need two linked copies");
+  const int G = GROUPS ? GROUPS : warp_groups(a0);
+  GSGP_REQUIRE(G >= 1 && G <= a0.max_groups, "not enough linked program copies for the genome groups");
+  InterpArgs a = a0;
+  a.exe_gstride = a.count * a.exe_k1;   // group copies of this launch's linked programs
   const int64_t ntiles = (a.nq + TILE - 1) / TILE;
   GSGP_REQUIRE(a.te_q >= a.ntr && (a.nte == 0 || a.te_q % TILE == 0 || a.te_q == a.ntr),
                "test cases must start on an interpreter tile");
   GSGP_REQUIRE(a.q_base % TILE == 0 && a.q_base + a.nq <= a.te_q + a.nte, "bad interpreter case range");
   const uint32_t rowb = TILE * 8;
   const uint32_t frows = kXSmem ? (uint32_t)a.l : 0u;
-  const size_t smem = cfg_smem(c, a);
-  GSGP_REQUIRE(smem <= kSmemCap, "interpreter tile does not fit in shared memory");
+  const size_t smem = cfg_smem(c, a, G);
+  GSGP_REQUIRE(smem <= (GROUPS ? kSmemCap : kSmemCapWarps), "interpreter tile does not fit in shared memory");
   // link the programs for this row layout
   const uint32_t grows = (uint32_t)cfg_group_rows(c, a);
   k_link<<<(unsigned)((a.count + 3) / 4), 128, 0, s>>>(a.code, a.exe, a.len, a.count, a.k1, NT, rowb,
-                                                      frows, (uint32_t)a.maxdepth, kLean, GROUPS, grows,
-                                                      a.exe_gstride);
+                                                      frows, (uint32_t)a.maxdepth, kLean, G, grows,
+                                                      a.exe_gstride, a.exe_k1);
   GSGP_CUDA(cudaGetLastError());
   // genomes per block: enough blocks to fill 148 SMs several times over
-  const int64_t want = 148 * 8;
+  // (one-warp groups: one block per SM, genomes per block a multiple of G)
+  const int64_t want = GROUPS ? 148 * 8 : 148 * 16;
   int64_t gpb = (a.count * ntiles + want - 1) / want;
-  if (gpb < 1) gpb = 1;
-  if (gpb > 64) gpb = 64;
+  if (GROUPS) {
+    gpb = std::max<int64_t>(1, std::min<int64_t>(gpb, 64));
+  } else {
+    gpb = std::max<int64_t>(gpb, G);
+    gpb = std::min<int64_t>((gpb + G - 1) / G * G, (a.count + G - 1) / G * G);
+  }
   const int64_t gy = (a.count + gpb - 1) / gpb;
   GSGP_REQUIRE(gy <= 65535, "too many genome groups");
   dim3 grid((unsigned)ntiles, (unsigned)gy);
   auto k = k_interpret<NT, CPT, MODE, TOut, kXSmem, kLean, GROUPS>;
   GSGP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k<<<grid, NT * GROUPS, smem, s>>>(a, gpb, frows * rowb, (frows + (uint32_t)a.maxdepth) * rowb,
-                                    (uint32_t)cfg_rows_bytes(c, a), grows * rowb,
-                                    (uint32_t)cfg_prog_bytes(a));
+  k<<<grid, NT * G, smem, s>>>(a, gpb, frows * rowb, (frows + (uint32_t)a.maxdepth) * rowb,
+                               (uint32_t)cfg_rows_bytes(c, a, G), grows * rowb,
+                               (uint32_t)cfg_prog_bytes(a));
   GSGP_CUDA(cudaGetLastError());
 }
 
@@ -815,7 +858,7 @@ template <int MODE, typename TOut, int GROUPS>
 int resident_warps(const InterpArgs& a) {
   const InterpCfg& c = kCfgs[4 + GROUPS];
   const size_t sm = cfg_smem(c, a);
-  if (sm > kSmemCap || (GROUPS > 1 && a.exe_gstride <= 0)) return 0;
+  if (sm > kSmemCap || GROUPS > a.max_groups) return 0;
   auto k = k_interpret<128, 3, MODE, TOut, true, false, GROUPS>;
   int b = 0;
   GSGP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -848,6 +891,7 @@ void launch_mode(const InterpArgs& a, cudaStream_t s) {
     case 5: launch_cfg<128, 3, MODE, TOut, true>(a, s); break;
     case 6: launch_cfg<128, 3, MODE, TOut, true, false, 2>(a, s); break;
     case 7: launch_cfg<128, 4, MODE, TOut, true, false, 2>(a, s); break;
+    case kCfgWarps: launch_cfg<32, 4, MODE, TOut, true, false, 0>(a, s); break;
     default: launch_cfg<128, 1, MODE, TOut, false, true>(a, s); break;
   }
 }

@@ -71,13 +71,30 @@ void launch_compile(const uint8_t* tags, const int32_t* codes, const double* con
                     int32_t k, double eps, Program prog, cudaStream_t s);
 
 enum InterpMode : int { INTERP_F64 = 0, INTERP_POP = 1, INTERP_POOL = 2 };
-constexpr int kMaxInterpGroups = 2;   // genome groups per interpreter block (linked program copies)
+// linked-program scratch of the interpreter launches (relinked per launch):
+// `copies` group copies of `count` programs with stride k1 = maxlen + 1
+// (callers that allocate before compiling pass maxlen = k), at most 32 and
+// within ~1 GiB, and at least the register-feature blobs (2 * ng * (k + 1)
+// instructions)
+struct LinkedLayout { int64_t k1, ins; int32_t copies; };
+inline LinkedLayout linked_layout(int64_t count, int64_t ng, int64_t k, int32_t maxlen) {
+  LinkedLayout L;
+  L.k1 = (maxlen > 0 ? maxlen : 1) + 1;
+  const int64_t per = count * L.k1 * 16;
+  int64_t c = ((int64_t)1 << 30) / (per > 0 ? per : 1);
+  L.copies = (int32_t)(c < 2 ? 2 : (c > 32 ? 32 : c));
+  L.ins = L.copies * count * L.k1;
+  if (L.ins < 2 * ng * (k + 1)) L.ins = 2 * ng * (k + 1);
+  return L;
+}
 
 struct InterpArgs {
   const Ins* code;          // abstract program (count genomes, stride k1)
-  Ins* exe;                 // linked copy, rewritten by every launch_interpret
-  int64_t exe_gstride;      // elements between the per-group linked copies (0: one copy only;
-                            // grouped configurations need kMaxInterpGroups copies)
+  Ins* exe;                 // linked copies, rewritten by every launch_interpret (scratch)
+  int64_t exe_gstride;      // set by the launch: elements between the per-group linked copies
+  int64_t exe_k1;           // linked-program stride per genome (>= maxlen + 1)
+  int32_t max_groups;       // linked copies exe holds: max_groups * count * exe_k1 Ins
+                            // (and >= 2 * count * 2 * k1 for the register-feature blobs)
   const int32_t* len;
   const int32_t* nconst;
   const double* ctab;       // [count][k1 - 1]
