@@ -266,7 +266,7 @@ constexpr int kMaxWarpGroups = 24;
 int warp_groups(const InterpArgs& a) {
   const InterpCfg& c = kCfgs[kCfgWarps];
   const size_t base = cfg_smem(c, a, 0), per = cfg_smem(c, a, 1) - base;
-  int gmax = base < kSmemCapWarps ? (int)((kSmemCapWarps - base) / per) : 0;
+  int gmax = base < kSmemCapWarps && per > 0 ? (int)((kSmemCapWarps - base) / per) : 0;
   gmax = std::min(gmax, std::min(kMaxWarpGroups, (int)a.max_groups));
   return gmax >= 8 ? gmax : 0;
 }
