@@ -262,6 +262,12 @@ size_t cfg_smem(const InterpCfg& c, const InterpArgs& a, int groups) {
 // and the linked copies hold, at most kMaxWarpGroups warps (the kernel's
 // register budget: 80 at 24 warps); 0 if fewer than 8 fit
 constexpr size_t kSmemCapWarps = 220 * 1024;
+#ifndef GSGP_WARP_UNROLL
+#define GSGP_WARP_UNROLL 2
+#endif
+#ifndef GSGP_BLOCK_UNROLL
+#define GSGP_BLOCK_UNROLL 4
+#endif
 constexpr int kMaxWarpGroups = 24;
 int warp_groups(const InterpArgs& a) {
   const InterpCfg& c = kCfgs[kCfgWarps];
@@ -487,6 +493,12 @@ __global__ void __launch_bounds__(GROUPS ? NT * GROUPS : 32 * kMaxWarpGroups,
     for (int c = 0; c < CPT; ++c) acc[c] = 0.0;
     const uint4* gprog = reinterpret_cast<const uint4*>(a.exe + g * a.exe_k1);   // kLean
     uint4 nxt = kLean ? __ldg(gprog) : lds_u128(pbase);
+    // one-warp groups run every warp at its own program point, so the
+    // dispatch code is an instruction-cache working set: unrolled 2x there
+    // (1x: C3 1965 ms, 2x: 1840, 4x: 2410 — profiles/r02/interp); the
+    // block-wide groups keep the compiler's 4x
+    constexpr int kUnroll = NT == 32 ? GSGP_WARP_UNROLL : GSGP_BLOCK_UNROLL;
+#pragma unroll kUnroll
     for (int i = 0; i < len; ++i) {
       const uint4 in = nxt;
       // next instruction (smem holds len + 1; the HBM program has k + 1 >= len + 1 slots)
