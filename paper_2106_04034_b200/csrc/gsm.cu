@@ -510,6 +510,19 @@ RowLayout make_layout(int64_t ntr, int64_t nte, bool f64, bool allow_merge) {
 
 int64_t gsm_tile_cases(bool f64) { return kTileBytes / (f64 ? 8 : 4); }
 
+void gsm_preload() {   // see interp_preload
+  auto pre = [](auto k) {
+    cudaFuncAttributes f{};
+    GSGP_CUDA(cudaFuncGetAttributes(&f, k));
+  };
+  pre(k_gsm_tma<float, false>);
+  pre(k_gsm_tma<float, false, false, true>);
+  pre(k_gsm_tma<float, false, true>);
+  pre(k_gsm_tma<double, false>);
+  pre(k_gsm_tma<double, false, false, true>);
+  pre(k_gsm_tma<double, false, true>);
+}
+
 void launch_gsm(const GsmArgs& a, bool f64, bool operator_mode, cudaStream_t s) {
   launch_gsm_mode(a, f64, operator_mode ? 1 : 0, s);
 }

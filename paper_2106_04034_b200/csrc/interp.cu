@@ -908,7 +908,38 @@ void launch_mode(const InterpArgs& a, cudaStream_t s) {
   }
 }
 
+// CUDA loads a kernel lazily at its first launch (milliseconds for the large
+// dispatch kernels); interp_preload() loads every interpreter kernel of the
+// module up front so no timed stage of a run pays for it
+template <typename K>
+void preload_fn(K k) {
+  cudaFuncAttributes f{};
+  GSGP_CUDA(cudaFuncGetAttributes(&f, k));
+}
+template <int MODE, typename TOut>
+void preload_mode() {
+  preload_fn(k_interpret<128, 4, MODE, TOut, true, false, 1>);
+  preload_fn(k_interpret<64, 8, MODE, TOut, true, false, 1>);
+  preload_fn(k_interpret<128, 4, MODE, TOut, false, false, 1>);
+  preload_fn(k_interpret<128, 2, MODE, TOut, true, false, 1>);
+  preload_fn(k_interpret<128, 3, MODE, TOut, true, false, 1>);
+  preload_fn(k_interpret<128, 3, MODE, TOut, true, false, 2>);
+  preload_fn(k_interpret<128, 4, MODE, TOut, true, false, 2>);
+  preload_fn(k_interpret<32, 4, MODE, TOut, true, false, 0>);
+  preload_fn(k_interpret<128, 1, MODE, TOut, false, true, 1>);
+}
+
 }  // namespace
+
+void interp_preload() {
+  preload_fn(k_compile);
+  preload_fn(k_link);
+  preload_mode<INTERP_F64, double>();
+  preload_mode<INTERP_POP, float>();
+  preload_mode<INTERP_POP, double>();
+  preload_mode<INTERP_POOL, float>();
+  preload_mode<INTERP_POOL, double>();
+}
 
 void launch_compile(const uint8_t* tags, const int32_t* codes, const double* consts, int64_t count,
                     int32_t k, double eps, Program prog, cudaStream_t s) {

@@ -246,4 +246,9 @@ void launch_argminmax(const double* f, int64_t m, int64_t* out, cudaStream_t s);
 // elementwise fp64 sigmoid (mutation.py:32-34)
 void launch_sigmoid(const double* x, int64_t n, double* y, cudaStream_t s);
 
+// load the engine's interpreter / generation kernels into the current
+// device's context ahead of a run (CUDA lazy module loading)
+void interp_preload();
+void gsm_preload();
+
 }  // namespace gsgp
