@@ -412,6 +412,13 @@ __global__ void __launch_bounds__(GROUPS ? NT * GROUPS : 32 * kMaxWarpGroups,
   const int64_t q0 = a.q_base + l0;             // ... and as a shard stacked index
   const int64_t N = a.ntr + a.nte;
   __shared__ double red[64];
+  // one-warp groups claim genomes dynamically (block-local counter): warps
+  // that drew short programs take more, so a block ends within about one
+  // genome of its slowest warp (static round-robin left warps idle at the end
+  // of every block: one block per SM)
+  __shared__ unsigned claim;
+  if (GROUPS == 0 && threadIdx.x == 0) claim = 0;
+  if (GROUPS == 0) __syncthreads();
 
   if (kXSmem) {
     double* xs = reinterpret_cast<double*>(smem);
@@ -466,7 +473,16 @@ __global__ void __launch_bounds__(GROUPS ? NT * GROUPS : 32 * kMaxWarpGroups,
 
   const int64_t g0 = blockIdx.y * gpb;
   const int64_t g1 = min(a.count, g0 + gpb);
-  for (int64_t g = g0 + grp; g < g1; g += ngr) {
+  auto next_genome = [&](int64_t g) -> int64_t {
+    if constexpr (GROUPS == 0) {
+      unsigned c = 0;
+      if (tid == 0) c = atomicAdd(&claim, 1u);
+      return g0 + ngr + (int64_t)__shfl_sync(0xffffffffu, c, 0);
+    } else {
+      return g + ngr;
+    }
+  };
+  for (int64_t g = g0 + grp; g < g1; g = next_genome(g)) {
     // ---- stage genome g: program + constant table (replicated for the CPT
     // cases of a thread) into shared memory
     const int len = a.len[g];
