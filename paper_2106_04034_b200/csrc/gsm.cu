@@ -82,7 +82,7 @@ __device__ __forceinline__ UnitSpan unit_span(int64_t t, const RowLayout& L) {
 #define GSGP_GSM_STAGES 4
 #endif
 #ifndef GSGP_GSM_CWARPS
-#define GSGP_GSM_CWARPS 16
+#define GSGP_GSM_CWARPS 8   // 8 vs 16: C3 +2.7 %, C4 +5 %, C5 +3.6 % (profiles/r02/gsm)
 #endif
 constexpr int kTileBytes = GSGP_GSM_TILE;
 
@@ -94,7 +94,7 @@ constexpr int kTileBytes = GSGP_GSM_TILE;
 // case tiles in lockstep and each pool tile is fetched from HBM once, then
 // re-served from L2 to every row that references it (pool copies: L2
 // evict_last; parent: evict_first; offspring stores: streaming).
-//   warp W  producer (W = kConsumerWarps, 16 by default): claims batches
+//   warp W  producer (W = kConsumerWarps, 8 by default): claims batches
 //           of units, the warp's lanes draw the rows' mutation plans
 //           (u, v, ms) from the counter RNG in parallel, and one lane issues
 //           3 cp.async.bulk copies (parent row tile, pool[u] tile, pool[v]
