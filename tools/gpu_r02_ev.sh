@@ -2,7 +2,7 @@
 # full ncu captures of GSM / interpreter / reduce-survive at C2, C3 GSM DRAM traffic,
 # C4/C5 bench lines, tail probe.
 set -x
-E=gpurun_out/r02/ev
+E=gpurun_out/${EV:-r02/ev}
 mkdir -p $E
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks.mem,power.limit --format=csv > $E/gpu_info.csv
 lscpu | grep -E "Model name|^CPU\(s\)" > $E/cpu_info.txt

@@ -24,7 +24,7 @@ def main(path):
             runs.append(cur)
         if cur is None:
             continue
-        if name.startswith('k_gsm_tma<float, 0, 0>'):
+        if re.match(r'k_gsm_tma<float, 0, 0(, 0)?>', name):   # engine generation kernel (minus sign)
             cur["gsm"].append(us)
         elif name.startswith('k_reduce_survive'):
             cur["reduce"].append(us)
