@@ -21,7 +21,7 @@ CSRC = PKG / "csrc"
 OBJ = PKG / "_build"
 LIB = PKG / "libgsgp_b200.so"
 SOURCES = ["ops.cu", "interp.cu", "gsm.cu", "engine.cu", "capi.cu"]
-HEADERS = ["common.cuh", "kernels.cuh", "interp_dispatch.inc", "interp_rf_dispatch.inc"]
+HEADERS = ["common.cuh", "kernels.cuh", "interp_dispatch.inc"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

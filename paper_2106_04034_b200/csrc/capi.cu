@@ -217,7 +217,7 @@ int gsgp_compute_semantics(const uint8_t* tags, const int32_t* codes, const doub
     launch_compile(dt.as<uint8_t>(), dc.as<int32_t>(), dv.as<double>(), count, (int32_t)k, eps, prog, 0);
     int32_t maxima[4] = {0, 0, 0, 0};
     d2h(maxima, mx.p, 16);
-    const LinkedLayout ll = linked_layout(count, count, k, maxima[2]);
+    const LinkedLayout ll = linked_layout(count, maxima[2]);
     Buf exe(ll.ins * sizeof(Ins));
     Buf xr(n * l * 8), xt(n * l * 8), o(count * n * 8), nf(8);
     h2d(xr.p, X, n * l * 8);
@@ -246,7 +246,6 @@ int gsgp_compute_semantics(const uint8_t* tags, const int32_t* codes, const doub
     a.maxdepth = maxima[0];
     a.maxconst = maxima[1];
     a.maxlen = maxima[2];
-    a.maxwords = maxima[3];
     a.out64 = o.as<double>();
     a.nonfinite = nf.as<unsigned long long>();
     a.raw = replace_nonfinite ? 0 : 1;

@@ -568,7 +568,7 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   // linked programs: per-launch scratch, one copy per interpreter genome
   // group, sized for programs of up to k instructions (allocated here, before
   // the timed stages)
-  const LinkedLayout ll = linked_layout(std::max(m, r), ng, k, (int32_t)k);
+  const LinkedLayout ll = linked_layout(std::max(m, r), (int32_t)k);
   exe.alloc(ll.ins * sizeof(Ins));
   pnconst.alloc(ng * 4);
   ctab.alloc(ng * k * 8);
@@ -614,7 +614,7 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   launch_compile(tags.as<uint8_t>(), codes.as<int32_t>(), consts.as<double>(), ng, (int32_t)k,
                  cfg->division_eps, prog, st);
   GSGP_CUDA(cudaEventRecord(ev_compile1.e, st));
-  int32_t maxima[4] = {0, 0, 0, 0};   // {spill depth, constants, instructions, RF words}
+  int32_t maxima[4] = {0, 0, 0, 0};   // {spill depth, constants, instructions, unused}
   GSGP_CUDA(cudaMemcpyAsync(maxima, pmax.p, 16, cudaMemcpyDeviceToHost, st));
   // program lengths: one instruction per function node of the compiled tree
   // (the interpreter's work unit, reported as node evaluations per second)
@@ -668,7 +668,6 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
     ia.maxdepth = maxima[0];
     ia.maxconst = maxima[1];
     ia.maxlen = maxima[2];
-    ia.maxwords = maxima[3];
     ia.out = p->S.p;
     ia.out_is_f64 = f64 ? 1 : 0;
     ia.pitch = p->pitch;

@@ -36,7 +36,6 @@
 namespace gsgp {
 namespace {
 #include "interp_dispatch.inc"
-#include "interp_rf_dispatch.inc"
 }  // namespace
 }  // namespace gsgp
 
@@ -201,14 +200,6 @@ __global__ void k_compile(const uint8_t* __restrict__ tags, const int32_t* __res
   atomicMax(P.maxima, depth);
   atomicMax(P.maxima + 1, nc);
   atomicMax(P.maxima + 2, pc);
-  // register-feature program words (k_link_rf): L* expand to LOAD + OP,
-  // PUSHLOAD to PUSH + LOAD, P* to PUSH + LOAD + OP; padded to 4-word groups
-  int32_t rfw = 0;
-  for (int32_t i = 0; i < pc; ++i) {
-    const uint32_t kd = out[i].a & 0xff;
-    rfw += kd >= K_PADD ? 3 : (kd >= K_LADD || kd == K_PUSHLOAD ? 2 : 1);
-  }
-  atomicMax(P.maxima + 3, (rfw + 3) & ~3);
 }
 
 // ---------------------------------------------------------------- configurations
@@ -223,14 +214,13 @@ struct InterpCfg {
   int groups = 1;   // genome groups per block sharing one staged feature tile
                     // (each group: nt threads, its own spill/constant rows + program);
                     // 0: as many one-warp groups as shared memory holds (warp_groups)
-  bool rf = false;  // register-feature interpreter (k_interpret_rf, <= 8 features)
 };
 constexpr InterpCfg kCfgs[] = {{128, 4, true, false}, {64, 8, true, false}, {128, 4, false, false},
                                {128, 2, true, false}, {128, 1, false, true}, {128, 3, true, false},
                                {128, 3, true, false, 2}, {128, 4, true, false, 2},
-                               {128, 4, false, false, 1, true},
+                               {0, 0, false, false, 0},   // 8: retired (register-feature interpreter)
                                {32, 4, true, false, 0}};
-constexpr int kCfgRf = 8;
+constexpr int kCfgRetired = 8;
 constexpr int kCfgWarps = 9;   // one-warp genome groups on a 128-case feature tile
 constexpr int kNumCfgs = sizeof(kCfgs) / sizeof(kCfgs[0]);
 constexpr size_t kSmemCap = 200 * 1024;
@@ -247,14 +237,7 @@ size_t cfg_rows_bytes(const InterpCfg& c, const InterpArgs& a, int groups) {
 }
 // + 1 instruction per program: the loop prefetches one past the end
 size_t cfg_prog_bytes(const InterpArgs& a) { return (size_t)((a.maxlen > 0 ? a.maxlen : 1) + 1) * sizeof(Ins); }
-// register-feature configuration: two staged program blobs (double buffer)
-// + each warp's spill slots ([slot][case][lane] x 8 B)
-size_t rf_blob_bytes(const InterpArgs& a) {
-  const size_t b = 16 + 4 * (size_t)(a.maxwords > 4 ? a.maxwords : 4) + 8 * (size_t)(a.maxconst > 0 ? a.maxconst : 1);
-  return (b + 15) / 16 * 16;
-}
 size_t cfg_smem(const InterpCfg& c, const InterpArgs& a, int groups) {
-  if (c.rf) return 2 * rf_blob_bytes(a) + (size_t)(c.nt / 32) * (size_t)a.maxdepth * kRfSlotBytes;
   if (c.lean) return cfg_rows_bytes(c, a, groups) + 16;
   return cfg_rows_bytes(c, a, groups) + groups * cfg_prog_bytes(a);
 }
@@ -283,16 +266,10 @@ size_t cfg_smem(const InterpCfg& c, const InterpArgs& a) {
 int choose_cfg(const InterpArgs& a) {
   const char* env = getenv("GSGP_INTERP_CFG");   // experiments / tests (read per launch)
   const int forced = env ? atoi(env) : -1;
-  const bool rf_ok = a.l <= kRfFeatures && a.maxwords > 0 && a.max_groups >= 2 &&
-                     rf_blob_bytes(a) <= (size_t)32 * a.k1 && cfg_smem(kCfgs[kCfgRf], a) <= kSmemCap;
   if (forced == kCfgWarps && warp_groups(a) > 0) return forced;
-  if (forced >= 0 && forced < kNumCfgs && forced != kCfgWarps && cfg_smem(kCfgs[forced], a) <= kSmemCap &&
-      kCfgs[forced].groups <= a.max_groups && (!kCfgs[forced].rf || rf_ok))
+  if (forced >= 0 && forced < kNumCfgs && forced != kCfgWarps && forced != kCfgRetired &&
+      cfg_smem(kCfgs[forced], a) <= kSmemCap && kCfgs[forced].groups <= a.max_groups)
     return forced;
-  // the register-feature interpreter (kCfgRf) is opt-in only: measured
-  // slower than the grouped shared-memory tiles at C2/C3 (C3 pop + pool
-  // 2224 vs 1768 ms, C2 13.7 vs 10.0 ms per launch: profiles/r02/README.md)
-  if (rf_ok && getenv("GSGP_INTERP_RF")) return kCfgRf;
   // two genome groups of 128 x 4 per block (cfg 7, compiled for 3 resident
   // blocks = 24 warps) when shared memory keeps 3 of them per SM: measured
   // 2.8 % faster at C3 than 128 x 3 groups with 32 warps (more cases per
@@ -630,253 +607,6 @@ void launch_cfg(const InterpArgs& a0, cudaStream_t s) {
   GSGP_CUDA(cudaGetLastError());
 }
 
-// ------------------------------------------------ register-feature interpreter
-// Datasets with at most 8 features (C1-C4): each thread keeps the features of
-// its 4 cases in registers, so a feature operand — the common one — costs no
-// memory access, and a program is a stream of 32-bit words, one jump per word
-// (tools/gen_interp_rf.py, interp_rf_dispatch.inc).  Blob of genome g at
-// exe + g * 32 * k1 bytes: {words (padded to 4), nconst, 0, 0}, the words,
-// then the genome's constants.
-
-// fast-path range of a constant operand, the same f32 test as the dispatch
-__device__ __forceinline__ bool rf_in_range(double v, float lo) {
-  const float h = fabsf(__uint_as_float((uint32_t)(__double_as_longlong(v) >> 32)));
-  return h >= lo && h < __uint_as_float(1524u << 20);
-}
-
-// word of an operation arm: op in {ADD SUB MUL RSUB DIV RDIV} (arm order) x source
-__device__ __forceinline__ uint32_t rf_op_word(uint32_t op, uint32_t cls, uint32_t idx, double cval, float dlo) {
-  const uint32_t base = RF_ADD_F0 + op * (kRfFeatures + 2);
-  if (cls == X_FEAT) return base + idx;
-  if (cls == X_STACK) return base + kRfFeatures + 1 + (idx << 8);
-  if (op == 4 && !rf_in_range(cval, dlo)) return RF_DIV_CS | (idx << 8);               // acc / c
-  if (op == 5 && !rf_in_range(cval, __uint_as_float(523u << 20))) return RF_RDIV_CS | (idx << 8);   // c / acc
-  return base + kRfFeatures + (idx << 8);
-}
-__device__ __forceinline__ uint32_t rf_load_word(uint32_t cls, uint32_t idx) {
-  return cls == X_FEAT ? RF_LOAD_F0 + idx : (RF_LOAD_C | (idx << 8));
-}
-
-// one warp per genome: expand the abstract program (k_compile) into words,
-// positions from a warp prefix sum, then append the constants
-__global__ void k_link_rf(const Ins* __restrict__ code, const int32_t* __restrict__ len,
-                          const int32_t* __restrict__ nconst, const double* __restrict__ ctab, int64_t count,
-                          int64_t k1, double eps, unsigned char* __restrict__ blobs) {
-  const int64_t g = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
-  if (g >= count) return;
-  const int lane = threadIdx.x % 32;
-  const int32_t n = len[g], nc = nconst[g];
-  const double* ct = ctab + g * (k1 - 1);
-  uint32_t* hdr = reinterpret_cast<uint32_t*>(blobs + g * 32 * k1);
-  uint32_t* words = hdr + 4;
-  const float dlo = __uint_as_float(max(523u << 20, (uint32_t)(__double_as_longlong(fabs(eps)) >> 32) + 1u));
-  // abstract kind -> arm operation (ADD SUB MUL DIV RSUB RDIV -> 0 1 2 4 3 5)
-  const uint32_t opmap[6] = {0, 1, 2, 4, 3, 5};
-  uint32_t pos = 0;
-  for (int32_t i0 = 0; i0 < n; i0 += 32) {
-    const int32_t i = i0 + lane;
-    uint32_t w[3] = {0, 0, 0}, nw = 0;
-    if (i < n) {
-      const Ins in = code[g * k1 + i];
-      const uint32_t kind = in.a & 0xff, xcls = (in.a >> 8) & 0xf, ycls = (in.a >> 12) & 0xf, push = in.a >> 16;
-      const double xv = xcls == X_CONST ? ct[in.b] : 0.0, yv = ycls == X_CONST ? ct[in.c] : 0.0;
-      if (kind <= K_RDIV) {
-        w[nw++] = rf_op_word(opmap[kind], xcls, in.b, xv, dlo);
-      } else if (kind == K_LOAD || kind == K_PUSHLOAD) {
-        if (kind == K_PUSHLOAD) w[nw++] = RF_PUSH | (push << 8);
-        w[nw++] = rf_load_word(xcls, in.b);
-      } else {                                   // L* / P*: [PUSH] LOAD x, OP y
-        if (kind >= K_PADD) w[nw++] = RF_PUSH | (push << 8);
-        w[nw++] = rf_load_word(xcls, in.b);
-        w[nw++] = rf_op_word(opmap[(kind - K_LADD) & 3], ycls, in.c, yv, dlo);
-      }
-    }
-    uint32_t incl = nw;                           // inclusive warp scan of the word counts
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += t;
-    }
-    const uint32_t at = pos + incl - nw;
-    for (uint32_t j = 0; j < nw; ++j) words[at + j] = w[j];
-    pos += __shfl_sync(0xffffffffu, incl, 31);
-  }
-  const uint32_t padded = (pos + 3) & ~3u;
-  for (uint32_t j = pos + lane; j < padded; j += 32) words[j] = RF_NOP;
-  double* cdst = reinterpret_cast<double*>(words + padded);
-  for (int32_t j = lane; j < nc; j += 32) cdst[j] = ct[j];
-  if (lane == 0) {
-    hdr[0] = padded;
-    hdr[1] = (uint32_t)nc;
-    hdr[2] = 0;
-    hdr[3] = 0;
-  }
-}
-
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-__device__ __forceinline__ uint32_t lds_u32(uint32_t p) {
-  uint32_t v;
-  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(p));
-  return v;
-}
-
-#ifndef GSGP_RF_MINB
-#define GSGP_RF_MINB 4
-#endif
-// 128 threads = 4 warps x 32 lanes x 4 cases: a 512-case tile; thread case c
-// is tile case warp*128 + c*32 + lane (coalesced feature loads and stores).
-// The block walks genomes [g0, g1) of its tile: the next genome's blob is
-// copied (cp.async) while the current one runs, one barrier per genome.
-template <int MODE, typename TOut>
-__global__ void __launch_bounds__(128, GSGP_RF_MINB) k_interpret_rf(InterpArgs a, int64_t gpb, uint32_t blob_bytes) {
-  constexpr int NT = 128, CPT = kRfCpt, TILE = NT * CPT;
-  extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ double red[2][NT / 32][2];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t tile = blockIdx.x;
-  const int64_t l0 = tile * TILE;
-  const int64_t q0 = a.q_base + l0;
-  const int64_t N = a.ntr + a.nte;
-  const unsigned char* blobs = reinterpret_cast<const unsigned char*>(a.exe);
-  const int64_t bstride = 32 * a.k1;
-
-  double f[kRfFeatures][CPT];
-  int64_t col[CPT];
-  double ytr[CPT];
-  bool valid[CPT], train[CPT];
-  uint32_t numok = 0, denok = 0;
-  const float dlo = __uint_as_float(max(523u << 20,
-      (uint32_t)(__double_as_longlong(fabs(a.eps)) >> 32) + 1u));
-#pragma unroll
-  for (int c = 0; c < CPT; ++c) {
-    const int64_t li = l0 + warp * (32 * CPT) + c * 32 + lane;     // launch-local case
-    const int64_t q = a.q_base + li;
-    train[c] = q < a.ntr;
-    valid[c] = li < a.nq && (train[c] || q >= a.te_q);
-    const int64_t j = q - a.te_q;
-    col[c] = train[c] ? q : (j < a.te_full ? a.test_off + j : a.tail_off + (j - a.te_full));
-    ytr[c] = (MODE == INTERP_POP && valid[c]) ? a.y[col[c]] : 0.0;
-#pragma unroll
-    for (int jf = 0; jf < kRfFeatures; ++jf) {
-      const double v = (jf < a.l && li < a.nq) ? a.XT[jf * a.xt_pitch + li] : 0.0;
-      f[jf][c] = v;
-      numok |= (rf_in_range(v, __uint_as_float(523u << 20)) ? 1u : 0u) << (4 * jf + c);
-      denok |= (rf_in_range(v, dlo) ? 1u : 0u) << (4 * jf + c);
-    }
-  }
-  uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
-  asm volatile("" : "+r"(sbase));
-  const uint32_t sp0 = sbase + 2 * blob_bytes + (uint32_t)warp * (uint32_t)a.maxdepth * kRfSlotBytes + lane * 8u;
-  unsigned long long nonfinite = 0;
-
-  const int64_t g0 = blockIdx.y * gpb;
-  const int64_t g1 = min(a.count, g0 + gpb);
-  auto stage = [&](int64_t g, int b) {
-    const unsigned char* src = blobs + g * bstride;
-    const uint32_t dst = sbase + (uint32_t)b * blob_bytes;
-    for (uint32_t o = (uint32_t)tid * 16u; o < blob_bytes; o += NT * 16u) cp_async16(dst + o, src + o);
-    cp_async_commit();
-  };
-  stage(g0, 0);
-  int buf = 0;
-  int64_t pend = -1;                 // genome whose tile SSE awaits the cross-warp sum
-  for (int64_t g = g0; g < g1; ++g) {
-    cp_async_wait_all();
-    __syncthreads();                 // blob g visible; every warp is done with the other buffer
-    if (MODE == INTERP_POP && pend >= 0 && tid < 2) {
-      double t = 0.0;
-      for (int w = 0; w < NT / 32; ++w) t = __dadd_rn(t, red[buf ^ 1][w][tid]);
-      a.part[(pend * a.part_ntiles + a.q_base / TILE + tile) * 2 + tid] = t;
-    }
-    if (g + 1 < g1) stage(g + 1, buf ^ 1);
-    const uint32_t pb = sbase + (uint32_t)buf * blob_bytes;
-    const uint32_t nw = lds_u32(pb);
-    const uint32_t cb = pb + 16u + 4u * nw;
-    double acc[CPT] = {0.0, 0.0, 0.0, 0.0};
-    uint32_t nxt = lds_u32(pb + 16u);
-#pragma unroll 1
-    for (uint32_t i = 0; i < nw; ++i) {
-      const uint32_t wd = nxt;
-      nxt = lds_u32(pb + 20u + 4u * i);             // one word past the end stays inside the blob buffer
-      rf_step(acc, f, wd, sp0, cb, a.eps, dlo, numok, denok);
-    }
-    // ---- epilogue: non-finite -> 0.0 counted (core.py:348-356), then store
-    double sse_tr = 0.0, sse_te = 0.0;
-    int wide = 0;
-#pragma unroll
-    for (int c = 0; c < CPT; ++c) {
-      if (!valid[c]) continue;
-      double v = acc[c];
-      if (!isfinite(v) && !(MODE == INTERP_F64 && a.raw)) { v = 0.0; ++nonfinite; }
-      if (MODE == INTERP_F64) {
-        a.out64[g * N + (q0 + warp * (32 * CPT) + c * 32 + lane)] = v;
-      } else if (MODE == INTERP_POP) {
-        const TOut o = (TOut)v;
-        reinterpret_cast<TOut*>(a.out)[g * a.pitch + col[c]] = o;
-        if (isinf((double)o)) wide |= train[c] ? 1 : 2;
-        const double d = __dsub_rn(v, ytr[c]);
-        if (train[c]) sse_tr = __dadd_rn(sse_tr, __dmul_rn(d, d));
-        else sse_te = __dadd_rn(sse_te, __dmul_rn(d, d));
-      } else {
-        const double sg = __ddiv_rn(1.0, __dadd_rn(1.0, exp(-v)));   // mutation.py:32-34
-        reinterpret_cast<TOut*>(a.out)[g * a.pitch + col[c]] = (TOut)sg;
-      }
-    }
-    if (MODE == INTERP_POP) {
-      sse_tr = warp_sum(sse_tr);
-      sse_te = warp_sum(sse_te);
-      const int wb = __reduce_or_sync(0xffffffffu, wide);
-      if (lane == 0) {
-        red[buf][warp][0] = sse_tr;
-        red[buf][warp][1] = sse_te;
-        if (wb) atomicOr(a.wide + g, wb);
-      }
-      pend = g;
-    }
-    buf ^= 1;
-  }
-  if (MODE == INTERP_POP && pend >= 0) {
-    __syncthreads();
-    if (tid < 2) {
-      double t = 0.0;
-      for (int w = 0; w < NT / 32; ++w) t = __dadd_rn(t, red[buf ^ 1][w][tid]);
-      a.part[(pend * a.part_ntiles + a.q_base / TILE + tile) * 2 + tid] = t;
-    }
-  }
-  for (int o = 16; o > 0; o >>= 1) nonfinite += __shfl_xor_sync(0xffffffffu, nonfinite, o);
-  if (lane == 0 && nonfinite) atomicAdd(a.nonfinite, nonfinite);
-}
-
-template <int MODE, typename TOut>
-void launch_rf(const InterpArgs& a, cudaStream_t s) {
-  constexpr int TILE = 128 * kRfCpt;
-  const int64_t ntiles = (a.nq + TILE - 1) / TILE;
-  GSGP_REQUIRE(a.l <= kRfFeatures, "register-feature interpreter: at most 8 features");
-  GSGP_REQUIRE(a.te_q >= a.ntr && (a.nte == 0 || a.te_q % TILE == 0 || a.te_q == a.ntr),
-               "test cases must start on an interpreter tile");
-  GSGP_REQUIRE(a.q_base % TILE == 0 && a.q_base + a.nq <= a.te_q + a.nte, "bad interpreter case range");
-  const size_t blob = rf_blob_bytes(a);
-  const size_t smem = cfg_smem(kCfgs[kCfgRf], a);
-  GSGP_REQUIRE(smem <= kSmemCap && blob <= (size_t)32 * a.k1, "register-feature program does not fit");
-  k_link_rf<<<(unsigned)((a.count + 3) / 4), 128, 0, s>>>(a.code, a.len, a.nconst, a.ctab, a.count, a.k1, a.eps,
-                                                         reinterpret_cast<unsigned char*>(a.exe));
-  GSGP_CUDA(cudaGetLastError());
-  const int64_t want = 148 * 8;
-  int64_t gpb = (a.count * ntiles + want - 1) / want;
-  if (gpb < 1) gpb = 1;
-  if (gpb > 64) gpb = 64;
-  const int64_t gy = (a.count + gpb - 1) / gpb;
-  GSGP_REQUIRE(gy <= 65535, "too many genome groups");
-  auto k = k_interpret_rf<MODE, TOut>;
-  GSGP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k<<<dim3((unsigned)ntiles, (unsigned)gy), 128, smem, s>>>(a, gpb, (uint32_t)blob);
-  GSGP_CUDA(cudaGetLastError());
-}
-
 // 128x3 tiles: 1 or 2 genome groups per block (cfg 5, 6) share the staged
 // feature tile; when shared memory limits the resident blocks the grouped
 // launch holds more warps per SM.  The occupancy calculator picks the one
@@ -911,7 +641,6 @@ void launch_mode(const InterpArgs& a, cudaStream_t s) {
   int cfg = choose_cfg(a);
   if (cfg == 5) cfg = grouped_or_single<MODE, TOut>(a);
   switch (cfg) {
-    case kCfgRf: launch_rf<MODE, TOut>(a, s); break;
     case 0: launch_cfg<128, 4, MODE, TOut, true>(a, s); break;
     case 1: launch_cfg<64, 8, MODE, TOut, true>(a, s); break;
     case 2: launch_cfg<128, 4, MODE, TOut, false>(a, s); break;

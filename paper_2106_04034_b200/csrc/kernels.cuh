@@ -59,8 +59,7 @@ struct Program {
   int32_t* len;         // [count] instructions
   int32_t* nconst;      // [count] constant-table entries
   double* ctab;         // [count][k] constants referenced by the program
-  int32_t* maxima;      // [4] {spill depth, constants, instructions, register-feature
-                        // program words (interp_rf_dispatch.inc)}: max over genomes
+  int32_t* maxima;      // [4] {spill depth, constants, instructions, unused}: max over genomes
   int32_t* scratch;     // [count][4*k] ints
   uint8_t* flags;       // [count][k]
   double* cval;         // [count][k]
@@ -73,18 +72,16 @@ void launch_compile(const uint8_t* tags, const int32_t* codes, const double* con
 enum InterpMode : int { INTERP_F64 = 0, INTERP_POP = 1, INTERP_POOL = 2 };
 // linked-program scratch of the interpreter launches (relinked per launch):
 // `copies` group copies of `count` programs with stride k1 = maxlen + 1
-// (callers that allocate before compiling pass maxlen = k), at most 32 and
-// within ~1 GiB, and at least the register-feature blobs (2 * ng * (k + 1)
-// instructions)
+// (callers that allocate before compiling pass maxlen = k), at least 2, at
+// most 32, and within ~1 GiB beyond 2
 struct LinkedLayout { int64_t k1, ins; int32_t copies; };
-inline LinkedLayout linked_layout(int64_t count, int64_t ng, int64_t k, int32_t maxlen) {
+inline LinkedLayout linked_layout(int64_t count, int32_t maxlen) {
   LinkedLayout L;
   L.k1 = (maxlen > 0 ? maxlen : 1) + 1;
   const int64_t per = count * L.k1 * 16;
   int64_t c = ((int64_t)1 << 30) / (per > 0 ? per : 1);
   L.copies = (int32_t)(c < 2 ? 2 : (c > 32 ? 32 : c));
   L.ins = L.copies * count * L.k1;
-  if (L.ins < 2 * ng * (k + 1)) L.ins = 2 * ng * (k + 1);
   return L;
 }
 
@@ -94,14 +91,12 @@ struct InterpArgs {
   int64_t exe_gstride;      // set by the launch: elements between the per-group linked copies
   int64_t exe_k1;           // linked-program stride per genome (>= maxlen + 1)
   int32_t max_groups;       // linked copies exe holds: max_groups * count * exe_k1 Ins
-                            // (and >= 2 * count * 2 * k1 for the register-feature blobs)
   const int32_t* len;
   const int32_t* nconst;
   const double* ctab;       // [count][k1 - 1]
   int64_t k1;               // instruction stride per genome (k + 1)
   int64_t count;            // genomes
   int32_t maxdepth, maxconst, maxlen;   // Program::maxima, read back once after compile
-  int32_t maxwords;                     // Program::maxima[3]
   const double* XT;         // [l][xt_pitch] fp64, feature-major: cases q_base .. q_base+nq-1
   int64_t xt_pitch;
   int32_t l;

@@ -55,9 +55,8 @@ def test_random_run_matches_engine_restatement(seed, monkeypatch):
         monkeypatch.setenv("GSGP_UPLOAD_CHUNK", "3072")
     # every interpreter launch configuration takes part (0 128x4, 2 HBM
     # features, 3 128x2, 4 lean, 5 128x3, 6/7 128x3/128x4 with two genome
-    # groups per block, 8 the register-feature interpreter, 9 one-warp genome
-    # groups on a 128-case tile)
-    monkeypatch.setenv("GSGP_INTERP_CFG", "0523467895"[seed % 10])
+    # groups per block, 9 one-warp genome groups on a 128-case tile)
+    monkeypatch.setenv("GSGP_INTERP_CFG", "052346795"[seed % 9])
     res = G.run_evolution(G.RunConfig(**kw), G.Dataset(Xtr, ytr), G.Dataset(Xte, yte),
                           virtual_shards=1 + seed % 3)
     o = engine32.run32(R.Cfg(**kw), Xtr, ytr, Xte, yte)
