@@ -219,7 +219,8 @@ constexpr InterpCfg kCfgs[] = {{128, 4, true, false}, {64, 8, true, false}, {128
                                {128, 2, true, false}, {128, 1, false, true}, {128, 3, true, false},
                                {128, 3, true, false, 2}, {128, 4, true, false, 2},
                                {0, 0, false, false, 0},   // 8: retired (register-feature interpreter)
-                               {32, 4, true, false, 0}};
+                               {32, 4, true, false, 0},
+                               {128, 4, true, false, 4}};
 constexpr int kCfgRetired = 8;
 constexpr int kCfgWarps = 9;   // one-warp genome groups on a 128-case feature tile
 constexpr int kNumCfgs = sizeof(kCfgs) / sizeof(kCfgs[0]);
@@ -275,6 +276,12 @@ int choose_cfg(const InterpArgs& a) {
   // 2.8 % faster at C3 than 128 x 3 groups with 32 warps (more cases per
   // dispatched instruction); the decision uses only shared memory, so it is
   // the same for every kernel instance and every rank
+  // four genome groups of 128 x 4 per block (cfg 10: 16 warps, compiled
+  // for 2 resident blocks = 32 warps at 64 registers, the epilogue state
+  // recomputed so the program loop keeps spills to a few words) when shared
+  // memory holds 2 of them: C2 20.0 -> 18.4 ms, C3 1770 -> 1688 ms, C4 233 ->
+  // 227 ms against cfg 7 (profiles/r02/interp/ab_groups4.log)
+  if (a.max_groups >= 4 && 2 * (cfg_smem(kCfgs[10], a) + 2048) <= 228 * 1024) return 10;
   if (a.max_groups >= 2 && 3 * (cfg_smem(kCfgs[7], a) + 2048) <= 228 * 1024) return 7;
   // features in shared memory while the tile keeps >= 3 blocks per SM; the
   // 384-case tile (128 x 3) fits 5 blocks (20 warps) where 128 x 4 fits 4:
@@ -369,7 +376,7 @@ __device__ __forceinline__ void group_sync(int grp) {
 // blockDim.x / NT groups (one-warp groups, NT == 32, sized at launch).
 template <int NT, int CPT, int MODE, typename TOut, bool kXSmem, bool kLean, int GROUPS>
 __global__ void __launch_bounds__(GROUPS ? NT * GROUPS : 32 * kMaxWarpGroups,
-                                  GROUPS == 2 ? (CPT == 3 ? GSGP_INTERP_MINB2 : 3) : 1) k_interpret(InterpArgs a, int64_t gpb,
+                                  GROUPS == 2 ? (CPT == 3 ? GSGP_INTERP_MINB2 : 3) : (GROUPS >= 3 ? 2 : 1)) k_interpret(InterpArgs a, int64_t gpb,
                                                            uint32_t stack_off, uint32_t crow_off,
                                                            uint32_t prog_off, uint32_t grp_bytes,
                                                            uint32_t prog_bytes) {
@@ -405,18 +412,20 @@ __global__ void __launch_bounds__(GROUPS ? NT * GROUPS : 32 * kMaxWarpGroups,
     }
     if (GROUPS != 1) __syncthreads();           // the groups only sync among themselves below
   }
-  double ytr[CPT];
-  int64_t col[CPT];
-  bool valid[CPT], train[CPT];
-#pragma unroll
-  for (int c = 0; c < CPT; ++c) {
+  // per-case bookkeeping of the epilogue, recomputed there (keeping it live
+  // through the program loop costs ~20 registers): case c of this thread is
+  // stacked case q0 + c * NT + tid; [ntr, te_q) is the test-start gap
+  auto is_valid = [&](int c) {
     const int64_t q = q0 + c * NT + tid;
-    train[c] = q < a.ntr;
-    valid[c] = l0 + c * NT + tid < a.nq && (train[c] || q >= a.te_q);   // [ntr, te_q): gap
-    const int64_t j = q - a.te_q;                       // test case index
-    col[c] = train[c] ? q : (j < a.te_full ? a.test_off + j : a.tail_off + (j - a.te_full));
-    ytr[c] = (MODE == INTERP_POP && valid[c]) ? a.y[col[c]] : 0.0;
-  }
+    return l0 + c * NT + tid < a.nq && (q < a.ntr || q >= a.te_q);
+  };
+  auto column = [&](int c) -> int64_t {     // storage column of case c
+    const int64_t q = q0 + c * NT + tid, j = q - a.te_q;
+    return q < a.ntr ? q : (j < a.te_full ? a.test_off + j : a.tail_off + (j - a.te_full));
+  };
+  uint32_t validm = 0;                      // HBM-feature fetches skip the cases past the range
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) validm |= is_valid(c) ? 1u << c : 0u;
   const double* xg = a.XT + l0 + tid;          // global feature rows (!kXSmem)
   uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
   asm volatile("" : "+r"(sbase));              // keep it in a register (no per-iteration remat)
@@ -440,7 +449,7 @@ __global__ void __launch_bounds__(GROUPS ? NT * GROUPS : 32 * kMaxWarpGroups,
     } else if (!kXSmem && (off & kFeatGlobal)) {
       const double* p = xg + (int64_t)(off & ~kFeatGlobal) * a.xt_pitch;
 #pragma unroll
-      for (int c = 0; c < CPT; ++c) v[c] = valid[c] ? __ldg(p + c * NT) : 0.0;
+      for (int c = 0; c < CPT; ++c) v[c] = (validm >> c & 1u) ? __ldg(p + c * NT) : 0.0;
     } else {
       const uint32_t p = sbase + off + (tid8 & mask);
 #pragma unroll
@@ -515,23 +524,25 @@ __global__ void __launch_bounds__(GROUPS ? NT * GROUPS : 32 * kMaxWarpGroups,
     int wide = 0;
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
-      if (!valid[c]) continue;
+      if (!(validm >> c & 1u)) continue;
       double v = acc[c];
       if (!isfinite(v) && !(MODE == INTERP_F64 && a.raw)) { v = 0.0; ++nonfinite; }
       const int64_t q = q0 + c * NT + tid;
       if (MODE == INTERP_F64) {
         a.out64[g * N + q] = v;
       } else if (MODE == INTERP_POP) {
+        const int64_t col = column(c);
+        const bool train = q < a.ntr;
         TOut o = (TOut)v;
-        reinterpret_cast<TOut*>(a.out)[g * a.pitch + col[c]] = o;
-        if (isinf((double)o)) wide |= train[c] ? 1 : 2;
-        double d = __dsub_rn(v, ytr[c]);
-        if (train[c]) sse_tr = __dadd_rn(sse_tr, __dmul_rn(d, d));
+        reinterpret_cast<TOut*>(a.out)[g * a.pitch + col] = o;
+        if (isinf((double)o)) wide |= train ? 1 : 2;
+        double d = __dsub_rn(v, __ldg(a.y + col));
+        if (train) sse_tr = __dadd_rn(sse_tr, __dmul_rn(d, d));
         else sse_te = __dadd_rn(sse_te, __dmul_rn(d, d));
       } else {
         // sigmoid of the pool, once per run (mutation.py:32-34, evolution.py:135-136)
         double sg = __ddiv_rn(1.0, __dadd_rn(1.0, exp(-v)));
-        reinterpret_cast<TOut*>(a.out)[g * a.pitch + col[c]] = (TOut)sg;
+        reinterpret_cast<TOut*>(a.out)[g * a.pitch + column(c)] = (TOut)sg;
       }
     }
     if (MODE == INTERP_POP) {
@@ -649,6 +660,7 @@ void launch_mode(const InterpArgs& a, cudaStream_t s) {
     case 6: launch_cfg<128, 3, MODE, TOut, true, false, 2>(a, s); break;
     case 7: launch_cfg<128, 4, MODE, TOut, true, false, 2>(a, s); break;
     case kCfgWarps: launch_cfg<32, 4, MODE, TOut, true, false, 0>(a, s); break;
+    case 10: launch_cfg<128, 4, MODE, TOut, true, false, 4>(a, s); break;
     default: launch_cfg<128, 1, MODE, TOut, false, true>(a, s); break;
   }
 }

@@ -409,7 +409,7 @@ def test_interpreter_division_fast_path_near_halfway_quotients():
     ref, _ = R.semantics(tags, codes, consts, X, 1e-6)
     pop = Population(tags, codes, consts)
     import os
-    for cfg in ("0", "1", "2", "3", "4", "5", "6", "7", "9"):
+    for cfg in ("0", "1", "2", "3", "4", "5", "6", "7", "9", "10"):
         os.environ["GSGP_INTERP_CFG"] = cfg
         try:
             S = G.compute_semantics(pop, X, RunConfig(program_size=k))
@@ -432,7 +432,7 @@ def test_dataset_split_matches_reference_golden():
 
 
 @pytest.mark.parametrize("count", [1, 2, 3, 5, 17])
-@pytest.mark.parametrize("cfg", ["5", "6", "7", "9"])
+@pytest.mark.parametrize("cfg", ["5", "6", "7", "9", "10"])
 def test_interpreter_genome_groups_with_odd_counts(count, cfg, monkeypatch):
     """Grouped interpreter blocks (cfg 6: two genome groups of 128 threads
     per block sharing the feature tile) with genome counts that leave a
@@ -448,7 +448,7 @@ def test_interpreter_genome_groups_with_odd_counts(count, cfg, monkeypatch):
     assert np.array_equal(S.view(np.uint64), ref.view(np.uint64))
 
 
-@pytest.mark.parametrize("cfg", ["5", "7", "9"])
+@pytest.mark.parametrize("cfg", ["5", "7", "9", "10"])
 def test_interpreter_divisions_by_and_of_constants_and_spills(cfg, monkeypatch):
     """Divisions by and of constants (in range, and out of the fast path's
     range: 0, subnormal, tiny, huge, inf, near eps) and of spill operands:
@@ -536,7 +536,7 @@ def test_interpreter_division_by_constants_hard_operands(monkeypatch):
         with np.errstate(all="ignore"):
             ref, _ = R.semantics(tags, codes, consts, X, eps)
         ok = np.isfinite(ref)
-        for cfg in ("0", "1", "3", "5", "6", "7", "4", "9"):
+        for cfg in ("0", "1", "3", "5", "6", "7", "4", "9", "10"):
             monkeypatch.setenv("GSGP_INTERP_CFG", cfg)
             S = G.compute_semantics(pop, X, RunConfig(program_size=k, division_eps=eps))
             assert np.array_equal(S[ok].view(np.uint64), ref[ok].view(np.uint64)), (cfg, eps)

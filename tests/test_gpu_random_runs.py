@@ -55,8 +55,9 @@ def test_random_run_matches_engine_restatement(seed, monkeypatch):
         monkeypatch.setenv("GSGP_UPLOAD_CHUNK", "3072")
     # every interpreter launch configuration takes part (0 128x4, 2 HBM
     # features, 3 128x2, 4 lean, 5 128x3, 6/7 128x3/128x4 with two genome
-    # groups per block, 9 one-warp genome groups on a 128-case tile)
-    monkeypatch.setenv("GSGP_INTERP_CFG", "052346795"[seed % 9])
+    # groups per block, 9 one-warp genome groups on a 128-case tile, 10
+    # 128x4 with four genome groups per block)
+    monkeypatch.setenv("GSGP_INTERP_CFG", ["0", "5", "2", "3", "4", "6", "7", "9", "10", "5"][seed % 10])
     res = G.run_evolution(G.RunConfig(**kw), G.Dataset(Xtr, ytr), G.Dataset(Xte, yte),
                           virtual_shards=1 + seed % 3)
     o = engine32.run32(R.Cfg(**kw), Xtr, ytr, Xte, yte)
