@@ -59,6 +59,7 @@ CONFIGS = {
                 desc="C4-shaped profiling config: pop 8192, pool 1024, k=255, 100k+25k cases"),
 }
 METRIC = "generations/sec"
+L2_BYTES = 126 * 1024 * 1024     # B200 L2 (the timed semantics must not fit in it)
 NVML_REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
                 0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
                 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
@@ -152,6 +153,7 @@ def interp_line(res, c, world: int) -> dict:
     div = res.device.get("program_divisions") or {"population": 0, "pool": 0}
     fp64_ops = (ins["population"] + ins["pool"] + 7 * (div["population"] + div["pool"])) * N
     peak = fp64_peak()
+    smem = smem_roofline(res, N, t)
     return {"node_evals_per_s": evals / t if t > 0 else None, "unit": "function-node evals/s",
             "seconds": t, "mean_program_instructions": (ins["population"] + ins["pool"]) / (c["m"] + c["r"]),
             "division_share": (div["population"] + div["pool"]) / max(1, ins["population"] + ins["pool"]),
@@ -159,7 +161,46 @@ def interp_line(res, c, world: int) -> dict:
             "fp64_roofline": {"achieved": fp64_ops / t if t > 0 else None, "peak": peak["value"],
                               "unit": "fp64 lane-ops/s", "frac": fp64_ops / t / peak["value"] if t > 0 else None,
                               "ops": fp64_ops, "peak_source": peak["source"]},
-            "bound": "dispatch issue (see DESIGN.md §6)"}
+            "smem_roofline": smem,
+            "bound": "shared-memory operand wavefronts + dispatch issue (see DESIGN.md §6)"}
+
+
+# cases per thread and "features staged in shared memory" of the interpreter
+# launch configurations (interp.cu kCfgs; 8 is retired)
+INTERP_CFGS = {0: (4, True), 1: (8, True), 2: (4, False), 3: (2, True), 4: (1, False), 5: (3, True),
+               6: (3, True), 7: (4, True), 9: (4, True), 10: (4, True)}
+
+
+def smem_roofline(res, N: float, t: float):
+    """Shared-memory wavefronts (128 B each, one per SM per clock) the
+    interpreter's operand traffic needs, from the compiled programs' op mix
+    (k_compile): per warp-instruction one broadcast LDS.128 program fetch, 2
+    wavefronts per case for a per-case operand load (feature or spill row:
+    32 lanes x 8 B) or spill store, 1 per case for a broadcast constant load.
+    Staging of features/programs/constants and bank conflicts are not
+    counted (ncu: the C2 population launch runs at 0.81 of the
+    l1tex shared-memory wavefront peak, profiles/r02/ncu_interp_src)."""
+    info = res.device.get("interpreter") or {}
+    ops = res.device.get("program_operands")
+    cfg = INTERP_CFGS.get(info.get("config"))
+    if not ops or cfg is None or not cfg[1] or t <= 0:
+        return None
+    cpt = cfg[0]
+    ins = res.device["program_instructions"]
+    per_warp = 0.0
+    for side in ("population", "pool"):
+        o = ops[side]
+        per_warp += ins[side] + cpt * (2 * o["vector_loads"] + o["constant_loads"] + 2 * o["spill_stores"])
+    wf = per_warp * N / (32 * cpt)
+    try:
+        mhz = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["sm_max_mhz"])
+    except Exception:
+        mhz = 1965.0
+    peak = 148 * mhz * 1e6
+    return {"achieved": wf / t, "peak": peak, "unit": "shared-memory wavefronts/s (128 B)",
+            "frac": wf / t / peak, "wavefronts": wf,
+            "peak_source": f"1 wavefront per SM per clock at the {mhz:.0f} MHz max SM clock",
+            "cases_per_thread": cpt}
 
 
 def fp64_peak() -> dict:
@@ -180,7 +221,7 @@ def workload_config(c) -> dict:
             "n_train": c["ntr"], "n_test": c["nte"],
             "l2": ("inputs larger than L2 (population and pool semantics "
                    f"{4 * c['m'] * (c['ntr'] + c['nte']) / 1e9:.1f} GB each)")
-            if c["ntr"] > 1_000_000 else "small config: L2-resident"}
+            if 4 * c["m"] * (c["ntr"] + c["nte"]) > L2_BYTES else "small config: L2-resident"}
 
 
 def ref_sample(c, max_cases=125_000):

@@ -86,6 +86,10 @@ typedef struct gsgp_outputs {
                                     programs' max spill depth, constants, instructions */
   int64_t interp_div[2];         /* out: protected-division instructions of the compiled
                                     population / random-tree programs (fp64 op mix) */
+  int64_t interp_ops[6];         /* out: operand traffic of the compiled population (0-2) /
+                                    random-tree (3-5) programs: per-case operand loads
+                                    (feature and spill rows), constant operand loads, spill
+                                    stores (the interpreter's shared-memory roofline) */
 } gsgp_outputs;
 
 const char* gsgp_version(void);

@@ -64,6 +64,7 @@ class GsgpOutputs(C.Structure):
         ("storage_f64_used", C.c_int64),
         ("interp_info", C.c_int64 * 4),
         ("interp_div", C.c_int64 * 2),
+        ("interp_ops", C.c_int64 * 6),
     ]
 
 

@@ -564,7 +564,7 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   consts.alloc(ng * k * 8);
   ins.alloc(ng * (k + 1) * sizeof(Ins));
   plen.alloc(ng * 4);
-  pndiv.alloc(ng * 4);
+  pndiv.alloc(ng * 16);   // [ng][4] op mix
   // linked programs: per-launch scratch, one copy per interpreter genome
   // group, sized for programs of up to k instructions (allocated here, before
   // the timed stages)
@@ -618,9 +618,9 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   GSGP_CUDA(cudaMemcpyAsync(maxima, pmax.p, 16, cudaMemcpyDeviceToHost, st));
   // program lengths: one instruction per function node of the compiled tree
   // (the interpreter's work unit, reported as node evaluations per second)
-  std::vector<int32_t> hlen(ng), hdiv(ng);
+  std::vector<int32_t> hlen(ng), hdiv(ng * 4);
   GSGP_CUDA(cudaMemcpyAsync(hlen.data(), plen.p, ng * 4, cudaMemcpyDeviceToHost, st));
-  GSGP_CUDA(cudaMemcpyAsync(hdiv.data(), pndiv.p, ng * 4, cudaMemcpyDeviceToHost, st));
+  GSGP_CUDA(cudaMemcpyAsync(hdiv.data(), pndiv.p, ng * 16, cudaMemcpyDeviceToHost, st));
   GSGP_CUDA(cudaStreamSynchronize(st));
 
   // pin_lease (this run's pinned upload staging) was taken before the timed
@@ -1048,7 +1048,12 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   out->stage_ms[18] = ins_pop;    // instructions (not ms): population programs
   out->stage_ms[19] = ins_pool;   // instructions: random-tree programs
   out->interp_div[0] = out->interp_div[1] = 0;
-  for (int64_t i = 0; i < ng; ++i) out->interp_div[i < m ? 0 : 1] += hdiv[i];
+  for (int q = 0; q < 6; ++q) out->interp_ops[q] = 0;
+  for (int64_t i = 0; i < ng; ++i) {
+    const int side = i < m ? 0 : 1;
+    out->interp_div[side] += hdiv[4 * i];
+    for (int q = 0; q < 3; ++q) out->interp_ops[3 * side + q] += hdiv[4 * i + 1 + q];
+  }
 }
 
 // ------------------------------------------------ single-process multi-GPU

@@ -189,13 +189,22 @@ __global__ void k_compile(const uint8_t* __restrict__ tags, const int32_t* __res
   }
   P.len[g] = pc;
   P.nconst[g] = nc;
-  if (P.ndiv) {   // op mix for the fp64 roofline (a division is 8 fp64 ops + MUFU)
-    int32_t nd = 0;
+  if (P.ndiv) {   // op mix for the rooflines (bench.py interp_line)
+    // [divisions (8 fp64 ops + MUFU each), per-case operand loads (feature /
+    //  spill rows), constant operand loads (broadcast), spill stores]
+    int32_t nd = 0, nv = 0, nk = 0, ns = 0;
     for (int32_t i = 0; i < pc; ++i) {
-      const uint32_t kd = out[i].a & 0xff;
+      const uint32_t a = out[i].a, kd = a & 0xff;
       nd += (kd == K_DIV || kd == K_RDIV || kd == K_LDIV || kd == K_PDIV) ? 1 : 0;
+      const uint32_t xc = (a >> 8) & 0xf, yc = (a >> 12) & 0xf;
+      (xc == X_CONST ? nk : nv) += 1;
+      if (kd >= K_LADD) (yc == X_CONST ? nk : nv) += 1;
+      ns += (kd == K_PUSHLOAD || kd >= K_PADD) ? 1 : 0;
     }
-    P.ndiv[g] = nd;
+    P.ndiv[4 * g] = nd;
+    P.ndiv[4 * g + 1] = nv;
+    P.ndiv[4 * g + 2] = nk;
+    P.ndiv[4 * g + 3] = ns;
   }
   atomicMax(P.maxima, depth);
   atomicMax(P.maxima + 1, nc);

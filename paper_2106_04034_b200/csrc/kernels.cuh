@@ -63,7 +63,7 @@ struct Program {
   int32_t* scratch;     // [count][4*k] ints
   uint8_t* flags;       // [count][k]
   double* cval;         // [count][k]
-  int32_t* ndiv;        // [count] protected-division instructions (DIV RDIV LDIV PDIV), or null
+  int32_t* ndiv;        // [count][4] op mix (divisions, vector / constant operand loads, spill stores), or null
 };
 // maxima[] must be zero before the launch (launch_compile clears it)
 void launch_compile(const uint8_t* tags, const int32_t* codes, const double* consts, int64_t count,

@@ -141,6 +141,10 @@ def run_evolution(cfg: RunConfig, train: Dataset, test: Dataset, *, storage: str
                           "alloc": st[17]},
               "program_instructions": {"population": int(st[18]), "pool": int(st[19])},
               "program_divisions": {"population": int(out.interp_div[0]), "pool": int(out.interp_div[1])},
+              "program_operands": {side: {"vector_loads": int(out.interp_ops[3 * j]),
+                                          "constant_loads": int(out.interp_ops[3 * j + 1]),
+                                          "spill_stores": int(out.interp_ops[3 * j + 2])}
+                                   for j, side in enumerate(("population", "pool"))},
               "devices": list(ids) if ids is not None else None,
               "storage": "fp64" if out.storage_f64_used else "fp32",
               "storage_requested": storage,
