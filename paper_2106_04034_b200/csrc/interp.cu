@@ -247,14 +247,27 @@ size_t cfg_rows_bytes(const InterpCfg& c, const InterpArgs& a, int groups) {
 }
 // + 1 instruction per program: the loop prefetches one past the end
 size_t cfg_prog_bytes(const InterpArgs& a) { return (size_t)((a.maxlen > 0 ? a.maxlen : 1) + 1) * sizeof(Ins); }
+// one-warp genome groups stage their program through a ring of two
+// kRingChunk-instruction chunks (+ one mirror slot, so the one-ahead
+// instruction fetch never wraps) refilled as the warp walks the program:
+// 1 KB per warp instead of the whole program (3.5 KB at k = 1024), so more
+// warps fit beside a wide feature tile
+constexpr int kRingChunk = 32;
+constexpr size_t kRingBytes = (2 * kRingChunk + 1) * sizeof(Ins);
+size_t cfg_group_prog_bytes(const InterpCfg& c, const InterpArgs& a) {
+  return c.groups == 0 ? kRingBytes : cfg_prog_bytes(a);
+}
 size_t cfg_smem(const InterpCfg& c, const InterpArgs& a, int groups) {
   if (c.lean) return cfg_rows_bytes(c, a, groups) + 16;
-  return cfg_rows_bytes(c, a, groups) + groups * cfg_prog_bytes(a);
+  return cfg_rows_bytes(c, a, groups) + groups * cfg_group_prog_bytes(c, a);
 }
 // one-warp genome groups: as many as the shared memory (one block per SM)
 // and the linked copies hold, at most kMaxWarpGroups warps (the kernel's
 // register budget: 80 at 24 warps); 0 if fewer than 8 fit
-constexpr size_t kSmemCapWarps = 220 * 1024;
+#ifndef GSGP_WARP_SMEM_KB
+#define GSGP_WARP_SMEM_KB 226   // 220: C5 pop+pool 654 ms, 226: 635 ms (profiles/r02/interp/ab_warp_smem_cap.log)
+#endif
+constexpr size_t kSmemCapWarps = GSGP_WARP_SMEM_KB * 1024;
 #ifndef GSGP_WARP_UNROLL
 #define GSGP_WARP_UNROLL 2
 #endif
@@ -483,11 +496,18 @@ __global__ void __launch_bounds__(GROUPS ? NT * GROUPS : 32 * kMaxWarpGroups,
     const int len = a.len[g];
     cg = a.ctab + g * cstride;
     group_sync<GROUPS, NT>(grp);                // previous genome done with both (and red[])
+    const uint4* psrc = reinterpret_cast<const uint4*>(a.exe + grp * a.exe_gstride + g * a.exe_k1);
+    uint4 pre = make_uint4(0u, 0u, 0u, 0u);   // ring: chunk 2 of the program, staged at chunk 1
     if (!kLean) {
     {
-      const uint4* src = reinterpret_cast<const uint4*>(a.exe + grp * a.exe_gstride + g * a.exe_k1);
       uint4* dst = reinterpret_cast<uint4*>(smem + prog_off);
-      for (int i = tid; i < len; i += NT) dst[i] = __ldg(src + i);
+      if constexpr (GROUPS == 0) {
+        for (int i = tid; i < 2 * kRingChunk; i += NT)
+          if (i < a.exe_k1) dst[i] = __ldg(psrc + i);
+        if (2 * kRingChunk + tid < a.exe_k1) pre = __ldg(psrc + 2 * kRingChunk + tid);
+      } else {
+        for (int i = tid; i < len; i += NT) dst[i] = __ldg(psrc + i);
+      }
       const int nc = a.nconst[g];
       const double* ct = a.ctab + g * cstride;
       for (int e = tid; e < nc * CPT; e += NT) {
@@ -509,11 +529,8 @@ __global__ void __launch_bounds__(GROUPS ? NT * GROUPS : 32 * kMaxWarpGroups,
     // (1x: C3 1965 ms, 2x: 1840, 4x: 2410 — profiles/r02/interp); the
     // block-wide groups keep the compiler's 4x
     constexpr int kUnroll = NT == 32 ? GSGP_WARP_UNROLL : GSGP_BLOCK_UNROLL;
-#pragma unroll kUnroll
-    for (int i = 0; i < len; ++i) {
-      const uint4 in = nxt;
-      // next instruction (smem holds len + 1; the HBM program has k + 1 >= len + 1 slots)
-      nxt = kLean ? __ldg(gprog + i + 1) : lds_u128(pbase + (uint32_t)(i + 1) * 16u);
+    // one program instruction over the CPT cases of this thread
+    auto step = [&](const uint4& in) {
       double x[CPT];
       fetch(in.y, in.w, x);
       const uint32_t kind = in.x;
@@ -527,6 +544,40 @@ __global__ void __launch_bounds__(GROUPS ? NT * GROUPS : 32 * kMaxWarpGroups,
         if (kind >= K_LADD) fetch(in.z, (in.w & 0x10000u) ? 0xffffffffu : 0u, y);   // second leaf
         Dispatch<CPT, CSTRIDE>::run(acc, x, y, kind, in.w, sp0, a.eps, dlo);
       }
+    };
+    if constexpr (GROUPS == 0) {
+      // program ring: chunk c lives in slot c & 1 (entry 2 * kRingChunk
+      // mirrors the first instruction of the even chunk in flight).  At the
+      // start of chunk c >= 1 the warp stores chunk c + 1 (loaded into
+      // registers one chunk earlier) over chunk c - 1 and loads chunk c + 2.
+      for (int i0 = 0; i0 < len; i0 += kRingChunk) {
+        if (i0 > 0) {
+          const int c = i0 / kRingChunk + 1;
+          __syncwarp();                                  // every lane is done with chunk c - 2's slot
+          uint4* ring = reinterpret_cast<uint4*>(smem + prog_off);
+          ring[(c & 1) * kRingChunk + tid] = pre;
+          if ((c & 1) == 0 && tid == 0) ring[2 * kRingChunk] = pre;
+          __syncwarp();
+          const int64_t nx = (int64_t)(c + 1) * kRingChunk + tid;
+          if (nx < a.exe_k1) pre = __ldg(psrc + nx);
+        }
+        const int jn = min(kRingChunk, len - i0);
+        const uint32_t rbase = pbase + (uint32_t)(i0 & (2 * kRingChunk - 1)) * 16u;
+#pragma unroll kUnroll
+        for (int j = 0; j < jn; ++j) {
+          const uint4 in = nxt;
+          nxt = lds_u128(rbase + (uint32_t)(j + 1) * 16u);
+          step(in);
+        }
+      }
+    } else {
+#pragma unroll kUnroll
+    for (int i = 0; i < len; ++i) {
+      const uint4 in = nxt;
+      // next instruction (smem holds len + 1; the HBM program has k + 1 >= len + 1 slots)
+      nxt = kLean ? __ldg(gprog + i + 1) : lds_u128(pbase + (uint32_t)(i + 1) * 16u);
+      step(in);
+    }
     }
     // ---- epilogue: non-finite -> 0.0 counted (core.py:348-356), then store
     double sse_tr = 0.0, sse_te = 0.0;
@@ -623,7 +674,7 @@ void launch_cfg(const InterpArgs& a0, cudaStream_t s) {
   GSGP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k<<<grid, NT * G, smem, s>>>(a, gpb, frows * rowb, (frows + (uint32_t)a.maxdepth) * rowb,
                                (uint32_t)cfg_rows_bytes(c, a, G), grows * rowb,
-                               (uint32_t)cfg_prog_bytes(a));
+                               (uint32_t)cfg_group_prog_bytes(c, a));
   GSGP_CUDA(cudaGetLastError());
 }
 
