@@ -742,6 +742,7 @@ void preload_mode() {
   preload_fn(k_interpret<128, 3, MODE, TOut, true, false, 1>);
   preload_fn(k_interpret<128, 3, MODE, TOut, true, false, 2>);
   preload_fn(k_interpret<128, 4, MODE, TOut, true, false, 2>);
+  preload_fn(k_interpret<128, 4, MODE, TOut, true, false, 4>);
   preload_fn(k_interpret<32, 4, MODE, TOut, true, false, 0>);
   preload_fn(k_interpret<128, 1, MODE, TOut, false, true, 1>);
 }
