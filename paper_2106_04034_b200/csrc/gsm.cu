@@ -302,7 +302,7 @@ k_gsm_tma(GsmArgs a, int64_t nunits, int kBatch) {
           if (k >= kStages) mbar_wait(empty + s, (j & 1) ^ 1);
           if (unit >= nunits) {
             slot_unit[s] = -1;
-            mbar_arrive(full + s);
+            mbar_expect_tx(full + s, 0);   // same completion path as a unit (0 transaction bytes)
           } else {
             const uint32_t bytes = (uint32_t)n * (uint32_t)sizeof(T);
             T* d = data + (int64_t)s * 3 * TILE;
@@ -372,7 +372,11 @@ k_gsm_tma(GsmArgs a, int64_t nunits, int kBatch) {
   unsigned long long nonfinite = 0;
   for (int64_t k = 0;; ++k) {
     mbar_wait(full + s, j & 1);
-    const int64_t unit = slot_unit[s];
+    // the stage's unit id: read by lane 0 (the lane that releases the stage)
+    // and broadcast
+    int64_t unit = 0;
+    if (lane == 0) unit = slot_unit[s];
+    unit = __shfl_sync(0xffffffffu, unit, 0);
     if (unit < 0) {   // no more units: tell the finalizer and stop
       if (lane == 0) {
         if (k >= kRedStages) mbar_wait(rempty + rs, (rj & 1) ^ 1);

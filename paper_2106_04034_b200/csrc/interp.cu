@@ -358,6 +358,9 @@ __global__ void k_link(const Ins* __restrict__ code, Ins* __restrict__ exe, cons
     o.d = (xvec ? 0x3ffu : 0u) | (yvec << 16) | (push << 20);
     exe[gi * gstride + g * exe_k1 + i] = o;
   }
+  // a zero instruction after the program: the interpreter prefetches one
+  // instruction past the end, and that read must see written memory
+  if (threadIdx.x % 32 == 0) exe[gi * gstride + g * exe_k1 + n] = Ins{0u, 0u, 0u, 0u};
   }
 }
 
@@ -502,11 +505,12 @@ __global__ void __launch_bounds__(GROUPS ? NT * GROUPS : 32 * kMaxWarpGroups,
     {
       uint4* dst = reinterpret_cast<uint4*>(smem + prog_off);
       if constexpr (GROUPS == 0) {
+        // (instructions 0..len: the program and the zero instruction after it)
         for (int i = tid; i < 2 * kRingChunk; i += NT)
-          if (i < a.exe_k1) dst[i] = __ldg(psrc + i);
-        if (2 * kRingChunk + tid < a.exe_k1) pre = __ldg(psrc + 2 * kRingChunk + tid);
+          if (i <= len) dst[i] = __ldg(psrc + i);
+        if (2 * kRingChunk + tid <= len) pre = __ldg(psrc + 2 * kRingChunk + tid);
       } else {
-        for (int i = tid; i < len; i += NT) dst[i] = __ldg(psrc + i);
+        for (int i = tid; i <= len; i += NT) dst[i] = __ldg(psrc + i);
       }
       const int nc = a.nconst[g];
       const double* ct = a.ctab + g * cstride;
@@ -559,7 +563,7 @@ __global__ void __launch_bounds__(GROUPS ? NT * GROUPS : 32 * kMaxWarpGroups,
           if ((c & 1) == 0 && tid == 0) ring[2 * kRingChunk] = pre;
           __syncwarp();
           const int64_t nx = (int64_t)(c + 1) * kRingChunk + tid;
-          if (nx < a.exe_k1) pre = __ldg(psrc + nx);
+          if (nx <= len) pre = __ldg(psrc + nx);
         }
         const int jn = min(kRingChunk, len - i0);
         const uint32_t rbase = pbase + (uint32_t)(i0 & (2 * kRingChunk - 1)) * 16u;
