@@ -1,0 +1,34 @@
+"""compute-sanitizer over tools/sanitize_paths.py, which drives every device
+kernel at tiny sizes (memcheck / racecheck / synccheck /
+initcheck on small configs): each tool must report zero errors."""
+
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = Path(__file__).resolve().parents[1]
+SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck", "initcheck"])
+def test_sanitizer_reports_no_errors(tool):
+    if not os.path.exists(SAN):
+        pytest.skip("compute-sanitizer not installed")
+    env = dict(os.environ)
+    env.pop("GSGP_INTERP_CFG", None)
+    p = subprocess.run([SAN, "--tool", tool, "--error-exitcode", "9", "--print-limit", "20",
+                        sys.executable, "tools/sanitize_paths.py"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=850)
+    out = p.stdout + p.stderr
+    assert p.returncode == 0, out[-4000:]
+    assert "sanitize paths ok" in out
+    assert ("ERROR SUMMARY: 0 errors" in out) or ("RACECHECK SUMMARY: 0 hazards" in out), out[-2000:]
