@@ -540,3 +540,51 @@ def test_interpreter_division_by_constants_hard_operands(monkeypatch):
             monkeypatch.setenv("GSGP_INTERP_CFG", cfg)
             S = G.compute_semantics(pop, X, RunConfig(program_size=k, division_eps=eps))
             assert np.array_equal(S[ok].view(np.uint64), ref[ok].view(np.uint64)), (cfg, eps)
+
+
+def _chain_genome(n_funcs: int, l: int, rng) -> tuple:
+    """A postfix chain f0 f1 op f2 op ... whose compiled program is exactly
+    n_funcs instructions (one leaf pair, then one accumulator op per
+    function), with every operator kind and feature/constant leaves."""
+    tags, codes, consts = [R.FEATURE, R.FEATURE], [0, 1 % l], [0.0, 0.0]
+    tags.append(R.FUNCTION)
+    codes.append(int(rng.integers(4)))
+    consts.append(0.0)
+    for _ in range(n_funcs - 1):
+        if rng.random() < 0.2:
+            tags.append(R.CONSTANT)
+            codes.append(0)
+            consts.append(float(rng.uniform(1, 10)))
+        else:
+            tags.append(R.FEATURE)
+            codes.append(int(rng.integers(l)))
+            consts.append(0.0)
+        tags.append(R.FUNCTION)
+        codes.append(int(rng.integers(4)))
+        consts.append(0.0)
+    return tags, codes, consts
+
+
+@pytest.mark.parametrize("cfg", ["9", "10"])
+def test_interpreter_program_ring_chunk_boundaries(cfg, monkeypatch):
+    """Programs whose compiled length sits on and around the one-warp groups'
+    32-instruction ring chunks (cfg 9 refills chunk c + 1 at the start of
+    chunk c) are bit-exact with the oracle; cfg 10 stages whole programs."""
+    rng = np.random.default_rng(7)
+    lengths = [1, 2, 31, 32, 33, 63, 64, 65, 95, 96, 97, 127, 128, 129, 200]
+    l, k = 5, 2 * max(lengths) + 2
+    rows = [_chain_genome(n, l, rng) for n in lengths]
+    tags = np.full((len(rows), k), R.CONSTANT, np.uint8)   # trailing constants: pushed, never the output
+    codes = np.zeros((len(rows), k), np.int32)
+    consts = np.ones((len(rows), k))
+    for i, (t, c, v) in enumerate(rows):
+        # the chain first, padded at the FRONT with constants that stay below
+        # the chain on the stack (the output is the last fired function)
+        off = k - len(t)
+        tags[i, off:], codes[i, off:], consts[i, off:] = t, c, v
+    X = rng.uniform(-2, 2, (700, l))
+    pop = Population(tags, codes, consts)
+    ref, _ = R.semantics(tags, codes, consts, X, 1e-6)
+    monkeypatch.setenv("GSGP_INTERP_CFG", cfg)
+    S = G.compute_semantics(pop, X, RunConfig(program_size=k))
+    assert np.array_equal(S.view(np.uint64), ref.view(np.uint64))
