@@ -2,7 +2,7 @@
 # C2/C4/C5 lines, ncu launch list of the default command, ncu full captures (C2 engine kernels),
 # C3 GSM DRAM bytes per launch.
 set -x
-O=gpurun_out/r02/ev3; mkdir -p $O
+O=gpurun_out/r02/${EV:-ev3}; mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks.mem,power.limit --format=csv > $O/gpu_info.csv
 lscpu | grep -E "Model name|^CPU\(s\)" > $O/cpu_info.txt
 timeout 1500 python -m pytest tests -q -m gpu --timeout 300 -p no:cacheprovider > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 $O/pytest_gpu.log
