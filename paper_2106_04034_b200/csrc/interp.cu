@@ -57,21 +57,38 @@ __device__ __forceinline__ Ins abstract_ins(uint32_t kind, uint32_t cls, uint32_
   return in;
 }
 
-// one thread per genome; scratch is per-genome global memory
+// one thread per genome.  Its working arrays (constant values, the stack,
+// child links, the emission work stack: 25 B per gene, and the flags) live in
+// shared memory when a few genomes' worth fit (k <= ~8k), else in per-genome
+// global scratch: the per-thread walks are latency-bound, and global scratch
+// went to L2 on every access (C1/C3 compile 1.3-1.4 ms, most of C1's init).
+constexpr size_t kCompileSmemCap = 192 * 1024;
+constexpr size_t compile_thread_bytes(int32_t k) { return ((size_t)k * (8 + 4 * 4 + 1) + 31) / 16 * 16; }
 __global__ void k_compile(const uint8_t* __restrict__ tags, const int32_t* __restrict__ codes,
                           const double* __restrict__ consts, int64_t count, int32_t k, double eps,
-                          Program P) {
+                          Program P, bool in_smem) {
+  extern __shared__ __align__(16) unsigned char csm[];
   int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (g >= count) return;
   const uint8_t* T = tags + g * k;
   const int32_t* C = codes + g * k;
   const double* V = consts + g * k;
-  int32_t* stk = P.scratch + g * 4 * (int64_t)k;
+  double* cv;
+  int32_t* stk;
+  uint8_t* fl;
+  if (in_smem) {
+    unsigned char* base = csm + threadIdx.x * compile_thread_bytes(k);
+    cv = reinterpret_cast<double*>(base);
+    stk = reinterpret_cast<int32_t*>(base + (size_t)k * 8);
+    fl = base + (size_t)k * 24;
+  } else {
+    cv = P.cval + g * (int64_t)k;
+    stk = P.scratch + g * 4 * (int64_t)k;
+    fl = P.flags + g * (int64_t)k;
+  }
   int32_t* Lc = stk + k;
   int32_t* Rc = Lc + k;
   int32_t* work = Rc + k;
-  uint8_t* fl = P.flags + g * (int64_t)k;
-  double* cv = P.cval + g * (int64_t)k;
   Ins* out = P.code + g * (int64_t)(k + 1);
   double* ctab = P.ctab + g * (int64_t)k;
 
@@ -767,7 +784,16 @@ void launch_compile(const uint8_t* tags, const int32_t* codes, const double* con
                     int32_t k, double eps, Program prog, cudaStream_t s) {
   if (count <= 0) return;
   GSGP_CUDA(cudaMemsetAsync(prog.maxima, 0, 4 * sizeof(int32_t), s));   // all four maxima
-  k_compile<<<(unsigned)((count + 63) / 64), 64, 0, s>>>(tags, codes, consts, count, k, eps, prog);
+  const size_t per = compile_thread_bytes(k);
+  const bool in_smem = per <= kCompileSmemCap / 2;
+  // shared-memory scratch: as many genomes per block as fit (<= 64), and at
+  // least two blocks' worth of genomes spread over the SMs
+  const int tpb = in_smem ? (int)std::min<size_t>(64, kCompileSmemCap / per) : 64;
+  const size_t smem = in_smem ? (size_t)tpb * per : 0;
+  if (in_smem)
+    GSGP_CUDA(cudaFuncSetAttribute(k_compile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_compile<<<(unsigned)((count + tpb - 1) / tpb), tpb, smem, s>>>(tags, codes, consts, count, k, eps, prog,
+                                                                   in_smem);
   GSGP_CUDA(cudaGetLastError());
 }
 
