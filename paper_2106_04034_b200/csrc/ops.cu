@@ -339,54 +339,83 @@ constexpr ArgVal kMaxInit{-INFINITY, INT64_MAX};
 // exchange, and the next generation's best parent needs no pass at all
 // (it is the elite slot: a parent elite is strictly below every offspring,
 // an offspring elite is the offspring minimum).
-__device__ void survive_block(const SurviveArgs& a) {
-  __shared__ ArgVal sh[3][32];
-  const int64_t m = a.m;
-  ArgVal bp = kMinInit, bo = kMinInit, wo = kMaxInit;
-  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
-    int32_t fl = a.wide[i];
-    double fo = (fl & 1) ? a.F[i] : rmse_of(a.sse_off[2 * i], a.ntr);
-    double to = (fl & 2) ? a.TS[i] : a.sse_off[2 * i + 1];
-    a.Fo[i] = fo;
-    a.To[i] = to;
-    bp = better_min(bp, ArgVal{a.F[i], i});
-    bo = better_min(bo, ArgVal{fo, i});
-    wo = better_max(wo, ArgVal{fo, i});
-  }
+// A candidate with the payload survival needs from its row: the parent
+// candidate carries its test SSE and slot flags (moved to the replaced slot
+// when a parent survives), the offspring candidate its test SSE (the trace).
+struct ArgPay {
+  double v;
+  int64_t i;
+  double ts;
+  int32_t fl;
+};
+template <bool kMin>
+__device__ __forceinline__ ArgPay pick(const ArgPay& a, const ArgPay& b) {
+  const bool take = kMin ? (b.v < a.v || (b.v == a.v && b.i < a.i)) : (b.v > a.v || (b.v == a.v && b.i < a.i));
+  return take ? b : a;
+}
+template <bool kMin>
+__device__ __forceinline__ ArgPay warp_pick(ArgPay x) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    ArgVal x{__shfl_xor_sync(0xffffffffu, bp.v, o), __shfl_xor_sync(0xffffffffu, bp.i, o)};
-    ArgVal y{__shfl_xor_sync(0xffffffffu, bo.v, o), __shfl_xor_sync(0xffffffffu, bo.i, o)};
-    ArgVal z{__shfl_xor_sync(0xffffffffu, wo.v, o), __shfl_xor_sync(0xffffffffu, wo.i, o)};
-    bp = better_min(bp, x);
-    bo = better_min(bo, y);
-    wo = better_max(wo, z);
+    ArgPay y{__shfl_xor_sync(0xffffffffu, x.v, o), __shfl_xor_sync(0xffffffffu, x.i, o),
+             __shfl_xor_sync(0xffffffffu, x.ts, o), __shfl_xor_sync(0xffffffffu, x.fl, o)};
+    x = pick<kMin>(x, y);
   }
+  return x;
+}
+
+// One pass over the rows: each thread reads its rows' parent state and
+// offspring SSE once, writes the next state (F, TS) in place and keeps the
+// three candidates (best parent, best and worst offspring) with their
+// payloads, so the block's leader finishes the generation from registers and
+// shared memory alone (no second pass over the rows; the replaced slot is the
+// only row it rewrites).
+__device__ void survive_block(const SurviveArgs& a) {
+  __shared__ ArgPay sh[3][32];
+  const int64_t m = a.m;
+  double* __restrict__ F = a.F;
+  double* __restrict__ TS = a.TS;
+  int32_t* __restrict__ wide = a.wide;
+  const double* __restrict__ sse = a.sse_off;
+  ArgPay bp{INFINITY, INT64_MAX, 0.0, 0}, bo{INFINITY, INT64_MAX, 0.0, 0}, wo{-INFINITY, INT64_MAX, 0.0, 0};
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+    const int32_t fl = wide[i];
+    const double fp = F[i], tsp = TS[i];
+    const double so = sse[2 * i], to_ = sse[2 * i + 1];
+    const double fo = (fl & 1) ? fp : rmse_of(so, a.ntr);
+    const double to = (fl & 2) ? tsp : to_;
+    bp = pick<true>(bp, ArgPay{fp, i, tsp, fl});
+    bo = pick<true>(bo, ArgPay{fo, i, to, 0});
+    wo = pick<false>(wo, ArgPay{fo, i, 0.0, 0});
+    F[i] = fo;                     // next state (the replaced slot is fixed below)
+    TS[i] = to;
+  }
+  bp = warp_pick<true>(bp);
+  bo = warp_pick<true>(bo);
+  wo = warp_pick<false>(wo);
   const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   if ((threadIdx.x & 31) == 0) { sh[0][w] = bp; sh[1][w] = bo; sh[2][w] = wo; }
-  __syncthreads();
+  __syncthreads();                 // also orders every row's F/TS write before the leader's
   if (threadIdx.x == 0) {
     bp = sh[0][0]; bo = sh[1][0]; wo = sh[2][0];
     for (int k = 1; k < nw; ++k) {
-      bp = better_min(bp, sh[0][k]);
-      bo = better_min(bo, sh[1][k]);
-      wo = better_max(wo, sh[2][k]);
+      bp = pick<true>(bp, sh[0][k]);
+      bo = pick<true>(bo, sh[1][k]);
+      wo = pick<false>(wo, sh[2][k]);
     }
-    int64_t g = a.ctl[CTL_GEN];
+    const int64_t g = a.ctl[CTL_GEN];
     int8_t src;
     int64_t idx, slot;
-    double fit;
+    double fit, ts;
     if (bp.v < bo.v) {                       // strict: exact ties keep the offspring
-      src = 0; idx = bp.i; slot = wo.i; fit = bp.v;
-      int32_t fl = a.wide[idx];
-      double ts = a.TS[idx];
-      a.Fo[slot] = fit;
-      a.To[slot] = ts;
-      a.wide[slot] = fl;
+      src = 0; idx = bp.i; slot = wo.i; fit = bp.v; ts = bp.ts;
+      F[slot] = fit;
+      TS[slot] = ts;
+      wide[slot] = bp.fl;
       a.ctl[CTL_REDIRECT] = slot;
       a.ctl[CTL_PARENT_ELITES] += 1;
     } else {
-      src = 1; idx = bo.i; slot = bo.i; fit = bo.v;
+      src = 1; idx = bo.i; slot = bo.i; fit = bo.v; ts = bo.ts;
       a.ctl[CTL_REDIRECT] = -1;
     }
     a.rec_src[g] = src;
@@ -394,15 +423,10 @@ __device__ void survive_block(const SurviveArgs& a) {
     a.rec_slot[g] = slot;
     a.rec_fit[g] = fit;
     a.trace_tr[g] = fit;
-    a.trace_te[g] = rmse_of(a.To[slot], a.nte);
+    a.trace_te[g] = rmse_of(ts, a.nte);
     a.ctl[CTL_BP] = slot;          // argmin of the surviving fitness vector
     a.ctl[CTL_PARITY] ^= 1;
     a.ctl[CTL_GEN] += 1;
-  }
-  __syncthreads();
-  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
-    a.F[i] = a.Fo[i];
-    a.TS[i] = a.To[i];
   }
 }
 
