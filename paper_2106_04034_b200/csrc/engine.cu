@@ -576,8 +576,8 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   scratch.alloc(ng * 4 * k * 4);
   flags.alloc(ng * k);
   cval.alloc(ng * k * 8);
-  DevBuf F, TS, Fo, To, wide, ctl, sse_total, nonfinite;
-  F.alloc(m * 8); TS.alloc(m * 8); Fo.alloc(m * 8); To.alloc(m * 8);
+  DevBuf F, TS, wide, ctl, sse_total, nonfinite;
+  F.alloc(m * 8); TS.alloc(m * 8);
   wide.alloc(m * 4);
   ctl.alloc(CTL_WORDS * 8);
   sse_total.alloc(m * 2 * 8);
@@ -875,8 +875,6 @@ void run_engine(const gsgp_config* cfg, const double* Xtr, const double* ytr, in
   sa.F = F.as<double>();
   sa.TS = TS.as<double>();
   sa.wide = wide.as<int32_t>();
-  sa.Fo = Fo.as<double>();
-  sa.To = To.as<double>();
   sa.ctl = ctl.as<int64_t>();
   sa.rec_src = rsrc.as<int8_t>();
   sa.rec_idx = ridx.as<int64_t>();

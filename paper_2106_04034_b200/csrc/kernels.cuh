@@ -212,8 +212,6 @@ struct SurviveArgs {
   double* F;                // [m] state train fitness (in: parent, out: next)
   double* TS;               // [m] state test SSE
   int32_t* wide;            // [m] slot flags
-  double* Fo;               // [m] scratch
-  double* To;               // [m] scratch
   int64_t* ctl;             // control block
   // lineage record for this generation (index = ctl[CTL_GEN])
   int8_t* rec_src; int64_t* rec_idx; int64_t* rec_slot; double* rec_fit;
